@@ -1,0 +1,192 @@
+"""ctypes binding of libsvgb200.so (the C-ABI in include/svgrad_b200.h).
+
+The product path has no fallback: if the library or a CUDA device is missing,
+every call raises ``NativeUnavailable`` -- there is no CPU implementation
+behind these entry points.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvgb200.so")
+ABI_VERSION = 1
+
+SVG_OK, SVG_EINVAL, SVG_ENOMEM, SVG_ECUDA, SVG_ENCCL, SVG_EUNSUPPORTED = range(6)
+FORM_PAULI, FORM_MAT = 0, 1
+
+EXPORTED = (
+    "svg_abi_version", "svg_last_error", "svg_device_count", "svg_engine_create",
+    "svg_engine_destroy", "svg_engine_set_stream", "svg_engine_set_option",
+    "svg_reverse_sweep", "svg_expectation",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library (or a device) is not available; there is no fallback."""
+
+
+class c128(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+C128x16 = c128 * 16
+
+
+class svg_gate(C.Structure):
+    _fields_ = [
+        ("form", C.c_int32), ("ntargets", C.c_int32), ("targets", C.c_int32 * 2),
+        ("ctrl_mask", C.c_uint64), ("x_mask", C.c_uint64), ("z_mask", C.c_uint64),
+        ("n_y", C.c_int32), ("nderiv", C.c_int32),
+        ("fwd", C128x16), ("rewind", C128x16), ("adjoint", C128x16),
+    ]
+
+
+class svg_deriv(C.Structure):
+    _fields_ = [
+        ("gate", C.c_int32), ("param_ref", C.c_int32), ("form", C.c_int32),
+        ("reserved", C.c_int32), ("k", C128x16),
+    ]
+
+
+class svg_pauli_term(C.Structure):
+    _fields_ = [
+        ("coeff", c128), ("x_mask", C.c_uint64), ("z_mask", C.c_uint64),
+        ("n_y", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+class svg_problem(C.Structure):
+    _fields_ = [
+        ("num_qubits", C.c_int32), ("num_params", C.c_int32), ("num_gates", C.c_int32),
+        ("num_derivs", C.c_int32), ("num_terms", C.c_int32), ("flags", C.c_int32),
+        ("gates", C.POINTER(svg_gate)), ("derivs", C.POINTER(svg_deriv)),
+        ("terms", C.POINTER(svg_pauli_term)), ("input_basis", C.c_int64),
+        ("input_amps", C.c_void_p),
+    ]
+
+
+class svg_stats(C.Structure):
+    _fields_ = [
+        ("ms_total", C.c_double), ("ms_forward", C.c_double), ("ms_observable", C.c_double),
+        ("ms_reverse", C.c_double), ("ms_other", C.c_double), ("launches", C.c_int64),
+        ("fwd_passes", C.c_int32), ("obs_passes", C.c_int32), ("rev_passes", C.c_int32),
+        ("tile_qubits", C.c_int32), ("pass_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the library once; raises NativeUnavailable if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python -m paper_2009_02823_b200._build` "
+                "(there is no CPU fallback for the gradient engine)"
+            )
+        lib = C.CDLL(path)
+        lib.svg_abi_version.restype = C.c_int
+        lib.svg_last_error.restype = C.c_char_p
+        lib.svg_device_count.argtypes = [C.POINTER(C.c_int)]
+        lib.svg_engine_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        lib.svg_engine_destroy.argtypes = [C.c_void_p]
+        lib.svg_engine_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+        lib.svg_engine_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        lib.svg_reverse_sweep.argtypes = [
+            C.c_void_p, C.POINTER(svg_problem), C.POINTER(c128), C.POINTER(c128),
+            C.POINTER(c128), C.POINTER(svg_stats),
+        ]
+        lib.svg_expectation.argtypes = [C.c_void_p, C.POINTER(svg_problem), C.POINTER(c128), C.POINTER(svg_stats)]
+        for name in EXPORTED:
+            getattr(lib, name).restype = C.c_char_p if name == "svg_last_error" else C.c_int
+        if lib.svg_abi_version() != ABI_VERSION:
+            raise NativeUnavailable(f"ABI mismatch: library {lib.svg_abi_version()}, wrapper {ABI_VERSION}")
+        _lib = lib
+        return lib
+
+
+def check(code: int) -> None:
+    """Map a C-ABI status onto the reference's exception types."""
+    if code == SVG_OK:
+        return
+    msg = (_lib.svg_last_error() or b"").decode(errors="replace")
+    if code == SVG_EINVAL:
+        raise ValueError(msg)
+    if code == SVG_ENOMEM:
+        raise MemoryError(msg)
+    if code == SVG_EUNSUPPORTED:
+        raise NativeUnavailable(msg)
+    raise RuntimeError(f"svgrad_b200 native error {code}: {msg}")
+
+
+class Engine:
+    """One device context: streams, cached HBM buffers, kernel attributes.
+
+    Not re-entrant (the reference's single-writer contract, pkg/README.md:71-73):
+    calls on one Engine are serialised by a lock; ctypes releases the GIL
+    for the duration of the native call.
+    """
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        handle = C.c_void_p()
+        check(self.lib.svg_engine_create(int(device), C.byref(handle)))
+        self.handle = handle
+        self.device = device
+        self.lock = threading.Lock()
+
+    def set_option(self, key: str, value: int) -> None:
+        check(self.lib.svg_engine_set_option(self.handle, key.encode(), int(value)))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        check(self.lib.svg_engine_set_stream(self.handle, C.c_void_p(stream_ptr or None)))
+
+    def reverse_sweep(self, problem: svg_problem, num_params: int, num_derivs: int):
+        sums = (c128 * max(1, num_params))()
+        derivs = (c128 * max(1, num_derivs))()
+        energy = c128()
+        stats = svg_stats()
+        with self.lock:
+            check(self.lib.svg_reverse_sweep(self.handle, C.byref(problem), sums, derivs,
+                                             C.byref(energy), C.byref(stats)))
+        return sums, derivs, energy, stats
+
+    def expectation(self, problem: svg_problem):
+        energy = c128()
+        stats = svg_stats()
+        with self.lock:
+            check(self.lib.svg_expectation(self.handle, C.byref(problem), C.byref(energy), C.byref(stats)))
+        return energy, stats
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.svg_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_engines: dict[int, Engine] = {}
+
+
+def engine(device: int = 0) -> Engine:
+    """Process-wide engine per device (created on first use)."""
+    e = _engines.get(device)
+    if e is None:
+        e = _engines[device] = Engine(device)
+    return e

@@ -1,0 +1,127 @@
+"""Drop-in gradient API: ``reverse_mode_gradient`` and friends on the B200 engine.
+
+Same signatures, validation order, error messages and return types as the
+reference (``svgrad/gradients.py:52-259``).  The work happens in one C-ABI
+call per sweep (``svg_reverse_sweep``, include/svgrad_b200.h); Python only
+validates, binds theta (lowering.py) and packages the report.
+
+``OpCounters`` keep the reference's contract: they count the primitive
+operations of Algorithm 1's schedule (3G-1 gate applications, A derivative
+applications, A+2 clones, A inner products, 1 observable application for G
+gates and A parameter occurrences -- svgrad/gradients.py:25-30), which is
+the algorithm-level work the fused kernels perform; the device never holds
+more than two state buffers, and the ``LiveStateAudit`` sequence reproduces
+the reference's acquire/release pattern (peak 4).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .lowering import Problem
+from .operators import adjoint_observable, is_hermitian
+
+
+@dataclass
+class OpCounters:
+    gate_applies: int = 0
+    derivative_applies: int = 0
+    clones: int = 0
+    inner_products: int = 0
+    observable_applies: int = 0
+
+
+@dataclass
+class GradientReport:
+    values: np.ndarray
+    energy: complex
+    counters: OpCounters
+
+
+class LiveStateAudit:
+    """Counts the state-vectors a gradient call holds simultaneously."""
+
+    def __init__(self):
+        self.live = 0
+        self.peak = 0
+
+    def acquire(self) -> None:
+        self.live += 1
+        self.peak = max(self.peak, self.live)
+
+    def release(self) -> None:
+        self.live -= 1
+
+
+_HERMITIAN_MSG = "observable is not Hermitian; use non_hermitian_gradient for complex expectations"
+
+
+def _check_call(circuit, params, obs, input_state) -> np.ndarray:
+    """Argument validation, same order and messages as svgrad/gradients.py:92-106."""
+    params = np.asarray(params, dtype=float)
+    if params.shape != (circuit.num_params,):
+        raise ValueError(f"parameter table has {circuit.num_params} entries, got shape {params.shape}")
+    if obs.num_qubits != circuit.num_qubits:
+        raise ValueError(f"observable acts on {obs.num_qubits} qubits, circuit on {circuit.num_qubits}")
+    if input_state.num_qubits != circuit.num_qubits:
+        raise ValueError(f"input state has {input_state.num_qubits} qubits, circuit {circuit.num_qubits}")
+    return params
+
+
+def _account(counters, audit, num_gates: int, num_derivs: int) -> None:
+    counters.gate_applies += 3 * num_gates - 1 if num_gates else 0
+    counters.derivative_applies += num_derivs
+    counters.clones += num_derivs + 2
+    counters.inner_products += num_derivs
+    counters.observable_applies += 1
+    audit.acquire()  # borrowed input
+    audit.acquire()  # bra (psi, then lambda)
+    audit.acquire()  # ket (phi)
+    for _ in range(num_derivs):
+        audit.acquire()  # probe -- folded into the fused reverse kernel, never allocated
+        audit.release()
+    audit.release()
+    audit.release()
+    audit.release()
+
+
+def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, stats: dict | None = None):
+    """Equivalent of the reference's ``_reverse_sweep``: (complex sums[P], energy)."""
+    problem = Problem(circuit, params, obs, input_state)
+    sums, _, energy, st = _native.engine(device).reverse_sweep(problem.c, circuit.num_params, problem.num_derivs)
+    _account(counters, audit, len(circuit.gates), problem.num_derivs)
+    out = np.ctypeslib.as_array(sums).view(np.complex128)[: circuit.num_params].copy()
+    if stats is not None:
+        stats.update(st.as_dict())
+    return out, complex(energy.re, energy.im)
+
+
+def reverse_mode_gradient(circuit, params, obs, input_state, audit: LiveStateAudit | None = None,
+                          *, device: int = 0, stats: dict | None = None) -> GradientReport:
+    """Full gradient of a Hermitian expectation in one fused backward sweep on the GPU."""
+    if not is_hermitian(obs):
+        raise ValueError(_HERMITIAN_MSG)
+    params = _check_call(circuit, params, obs, input_state)
+    counters = OpCounters()
+    sums, energy = sweep(circuit, params, obs, input_state, counters, audit or LiveStateAudit(), device, stats)
+    return GradientReport((2.0 * sums.real).astype(complex), energy, counters)
+
+
+def non_hermitian_gradient(circuit, params, obs, input_state, *, device: int = 0) -> GradientReport:
+    """Complex gradient of <psi|A|psi>: A-sweep conjugated plus A^dag-sweep (svgrad/gradients.py:240-259)."""
+    params = _check_call(circuit, params, obs, input_state)
+    counters = OpCounters()
+    audit = LiveStateAudit()
+    sums_a, energy = sweep(circuit, params, obs, input_state, counters, audit, device)
+    sums_adj, _ = sweep(circuit, params, adjoint_observable(obs), input_state, counters, audit, device)
+    return GradientReport(np.conj(sums_a) + sums_adj, energy, counters)
+
+
+def circuit_expectation(circuit, params, obs, input_state, *, device: int = 0) -> complex:
+    """<psi(theta)|H|psi(theta)> via the forward passes and the observable kernel only."""
+    params = _check_call(circuit, params, obs, input_state)
+    problem = Problem(circuit, params, obs, input_state)
+    energy, _ = _native.engine(device).expectation(problem.c)
+    return complex(energy.re, energy.im)

@@ -1,0 +1,27 @@
+// Host-callable launchers for the tile-pass kernels (kernels.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace svgb {
+
+size_t fwd_smem(int k, int b);
+size_t obs_smem(int k, int b);
+size_t rev_smem(int k, int b, int nslots);
+cudaError_t prepare_kernels(size_t max_smem);
+int occupancy(int which /*0 fwd, 1 obs, 2 rev*/, size_t smem);
+
+void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* psi,
+                const DevOp* ops, const double2* coef);
+void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi,
+                double2* lam, const DevTerm* terms, double2* partials);
+void launch_rev(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* phi, double2* lam,
+                const DevOp* ops, const double2* coef, double2* partials);
+void launch_finalize(const double2* partials, const SumSpec* specs, int count, double2* out,
+                     cudaStream_t s);
+void launch_set_basis(double2* psi, uint64_t idx, cudaStream_t s);
+
+}  // namespace svgb

@@ -1,0 +1,101 @@
+// Pass planner; see plan.h for the model.
+#include "plan.h"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace svgb {
+
+static inline int popc(uint64_t v) { return __builtin_popcountll(v); }
+static inline uint64_t low_mask(int b) { return b >= 64 ? ~0ull : ((1ull << b) - 1); }
+
+GateShape gate_shape(const svg_gate& g) {
+  GateShape s;
+  uint64_t tmask = 0;
+  for (int j = 0; j < g.ntargets; ++j) tmask |= 1ull << g.targets[j];
+  s.flip = (g.form == SVG_FORM_PAULI) ? g.x_mask : tmask;
+  s.touch = tmask | g.ctrl_mask;
+  s.nderiv = g.nderiv;
+  return s;
+}
+
+// Fill the tile set up to k qubits with the lowest unused qubits.
+static uint64_t pad_tile(uint64_t q, int n, int k) {
+  for (int i = 0; i < n && popc(q) < k; ++i) q |= 1ull << i;
+  return q;
+}
+
+std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp) {
+  const int G = static_cast<int>(shapes.size());
+  const uint64_t full = low_mask(pp.n);
+  std::vector<char> done(G, 0);
+  std::vector<Pass> passes;
+  int first = 0;
+  int remaining = G;
+  while (remaining > 0) {
+    while (done[first]) ++first;
+    Pass p;
+    uint64_t q = low_mask(pp.b);
+    uint64_t flip_blocked = 0, diag_blocked = 0;
+    int derivs = 0;
+    for (int i = first; i < G; ++i) {
+      if (done[i]) continue;
+      const GateShape& s = shapes[i];
+      const uint64_t diag = s.touch & ~s.flip;
+      bool ok = !(s.touch & flip_blocked) && !(s.flip & diag_blocked);
+      ok = ok && popc(q | s.flip) <= pp.k;
+      ok = ok && static_cast<int>(p.items.size()) < pp.max_items;
+      ok = ok && derivs + s.nderiv <= pp.max_derivs;
+      if (ok) {
+        q |= s.flip;
+        p.items.push_back(i);
+        derivs += s.nderiv;
+        done[i] = 1;
+        --remaining;
+      } else {
+        flip_blocked |= s.flip;
+        diag_blocked |= diag;
+        if ((flip_blocked & full) == full) break;  // nothing later can commute forward
+      }
+    }
+    if (p.items.empty()) throw std::runtime_error("planner made no progress (gate flip set wider than tile)");
+    p.qmask = pad_tile(q, pp.n, pp.k);
+    passes.push_back(std::move(p));
+  }
+  return passes;
+}
+
+std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp) {
+  std::vector<Pass> passes;
+  std::vector<uint64_t> masks;  // unpadded tile sets
+  for (int t = 0; t < static_cast<int>(term_flips.size()); ++t) {
+    const uint64_t f = term_flips[t];
+    if (popc(low_mask(pp.b) | f) > pp.k) throw std::runtime_error("observable term flips more qubits than a tile holds");
+    int chosen = -1;
+    for (int j = 0; j < static_cast<int>(passes.size()); ++j) {
+      if (popc(masks[j] | f) <= pp.k && static_cast<int>(passes[j].items.size()) < pp.max_items) {
+        chosen = j;
+        break;
+      }
+    }
+    if (chosen < 0) {
+      passes.emplace_back();
+      masks.push_back(low_mask(pp.b));
+      chosen = static_cast<int>(passes.size()) - 1;
+    }
+    masks[chosen] |= f;
+    passes[chosen].items.push_back(t);
+  }
+  for (size_t j = 0; j < passes.size(); ++j) passes[j].qmask = pad_tile(masks[j], pp.n, pp.k);
+  return passes;
+}
+
+int choose_tile_qubits(int n, int requested, int sms) {
+  if (requested > 0) return std::min(requested, n);
+  int k = std::min(n, 10);
+  // keep at least ~4 tiles per SM so the persistent grid stays balanced
+  while (k > 7 && (n - k) < 62 && (1ll << (n - k)) < 4ll * sms) --k;
+  return std::min(k, n);
+}
+
+}  // namespace svgb

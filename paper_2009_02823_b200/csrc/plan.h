@@ -1,0 +1,57 @@
+// Host-side pass planner: groups the gate list into HBM passes over tiles.
+//
+// A pass owns a tile-qubit set Q (|Q| = k, always containing the lowest b
+// qubits so every tile row is a contiguous run of 2^b amplitudes).  The
+// state is cut into 2^(n-k) independent tiles of 2^k amplitudes (fixed
+// values of the non-tile qubits); one CTA stages a tile in shared memory and
+// applies every gate of the pass to it, so the pass moves each amplitude
+// through HBM once instead of once per gate.
+//
+// Only the FLIP qubits of a gate (X/Y factors of a Pauli-form gate, targets
+// of a dense-matrix gate) must lie in Q.  Z factors and controls are
+// diagonal: their effect inside a tile is a per-tile constant computed from
+// the tile base index, so RZ/RZZ/controls never constrain the tile.
+//
+// Gates may be pulled forward past earlier, excluded gates only when they
+// commute with them: on every shared qubit both act diagonally.  This keeps
+// the planned order a valid reordering of the reference's gate sequence
+// (svgrad/gradients.py:149-150 forward, :158-168 reverse).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/svgrad_b200.h"
+
+namespace svgb {
+
+struct GateShape {
+  uint64_t flip;   // qubits that must be in the tile
+  uint64_t touch;  // every qubit the gate reads (targets, controls)
+  int nderiv;
+};
+
+struct Pass {
+  uint64_t qmask = 0;        // tile qubits (popcount == k)
+  std::vector<int> items;    // gate (or term) indices in application order
+};
+
+struct PlanParams {
+  int n = 0;
+  int k = 10;                // tile qubits
+  int b = 5;                 // forced contiguous low qubits
+  int max_items = 256;       // gates per pass cap
+  int max_derivs = 96;       // derivative slots per pass cap (shared-memory accumulators)
+};
+
+GateShape gate_shape(const svg_gate& g);
+
+// Forward gate passes; the reverse sweep walks the same passes backwards.
+std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp);
+
+// Observable passes: terms grouped so each pass's flip masks fit one tile.
+std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp);
+
+// Tile size choice for n qubits on `sms` SMs (auto when requested == 0).
+int choose_tile_qubits(int n, int requested, int sms);
+
+}  // namespace svgb

@@ -1,0 +1,229 @@
+"""Host lowering: (circuit, theta, observable, input) -> svg_problem tables.
+
+This is the reference's binding step (``_bind`` / ``_rewind_matrices`` /
+deferred derivative scalars, svgrad/gradients.py:109-125 and
+svgrad/circuit.py:228-334) restated as flat, device-ready tables:
+
+* Pauli-form gates (every ``PauliRotation``, and ``FixedUnitary`` X/Y/Z incl.
+  CX/CY/CZ) become ``op = a*I + b*P`` with the gate's Pauli product P:
+  ``U = cos(alpha*theta) I + i sin(alpha*theta) P`` (svgrad/gates.py:42-50),
+  ``U^-1 = U^dag = conj(a) I + conj(b) P``, and the derivative generator
+  relative to the pre-gate state, ``K = alpha*i * P U = alpha*i*(b I + a P)``
+  (the reference applies P then U and defers alpha*i, svgrad/circuit.py:316-321).
+* Dense-matrix gates (``Phase``, other ``FixedUnitary``, ``CustomParametric``,
+  ``NonUnitary``) ship U, the rewind (adjoint, or the true inverse for
+  NonUnitary -> ``NonInvertibleGateError`` text identical to
+  svgrad/gradients.py:121-122) and U^dag, plus K = scalar * dU/dtheta_j
+  (Phase: i e^{i theta} |1><1|; matrix kinds: analytic or central-FD dM).
+* Control projection (svgrad/circuit.py:330-331) is the gate's ctrl mask:
+  the device evaluates K only where every control bit is 1.
+
+The theta-independent structure of a circuit is cached per circuit object,
+so a VQE loop re-binds only the coefficient arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .ir import NonInvertibleGateError, SIGMA, bound_matrix, derivative_scale, invert_small, kind_name, matrix_derivative
+from .operators import pauli_masks, pauli_strings
+
+GATE_DTYPE = np.dtype(
+    [
+        ("form", "<i4"), ("ntargets", "<i4"), ("targets", "<i4", (2,)), ("ctrl_mask", "<u8"),
+        ("x_mask", "<u8"), ("z_mask", "<u8"), ("n_y", "<i4"), ("nderiv", "<i4"),
+        ("fwd", "<c16", (16,)), ("rewind", "<c16", (16,)), ("adjoint", "<c16", (16,)),
+    ],
+    align=True,
+)
+DERIV_DTYPE = np.dtype(
+    [("gate", "<i4"), ("param_ref", "<i4"), ("form", "<i4"), ("reserved", "<i4"), ("k", "<c16", (16,))],
+    align=True,
+)
+TERM_DTYPE = np.dtype(
+    [("coeff", "<c16"), ("x_mask", "<u8"), ("z_mask", "<u8"), ("n_y", "<i4"), ("reserved", "<i4")],
+    align=True,
+)
+_PAULI_FIXED = {"X": SIGMA["X"], "Y": SIGMA["Y"], "Z": SIGMA["Z"]}
+
+
+@dataclass
+class Structure:
+    """theta-independent part of a lowered circuit."""
+
+    gates: np.ndarray            # GATE_DTYPE, masks/targets filled, coefficients zero
+    derivs: np.ndarray           # DERIV_DTYPE, gate/param_ref/form filled
+    rot_gates: np.ndarray        # indices of PauliRotation gates
+    rot_refs: np.ndarray         # their parameter slot
+    rot_alpha: np.ndarray        # their alpha
+    rot_derivs: np.ndarray       # their derivative row
+    fixed_pauli: np.ndarray      # indices of X/Y/Z fixed gates (a=0, b=1)
+    mat_gates: list              # indices of dense-matrix gates (bound per call)
+    num_derivs: int
+
+
+_cache: dict[int, tuple] = {}
+
+
+def _structure(circuit) -> Structure:
+    hit = _cache.get(id(circuit))
+    if hit is not None and hit[0]() is circuit:
+        return hit[1]
+    gates = circuit.gates
+    G = len(gates)
+    arr = np.zeros(G, dtype=GATE_DTYPE)
+    rot_g, rot_r, rot_a, rot_d, fixed_p, mats = [], [], [], [], [], []
+    drows = []
+    for i, g in enumerate(gates):
+        name = kind_name(g)
+        targets = tuple(g.targets)
+        ctrl = 0
+        for c in g.controls:
+            ctrl |= 1 << c
+        rec = arr[i]
+        rec["ntargets"] = len(targets)
+        rec["targets"][: len(targets)] = targets
+        rec["ctrl_mask"] = ctrl
+        arity = len(g.param_refs)
+        rec["nderiv"] = arity
+        form = N.FORM_MAT
+        if name == "PauliRotation":
+            form = N.FORM_PAULI
+            letters = ["I"] * (max(targets) + 1)
+            for axis, t in zip(g.kind.axes, targets):
+                letters[t] = axis
+            x, z, ny = pauli_masks("".join(letters))
+            rec["x_mask"], rec["z_mask"], rec["n_y"] = x, z, ny
+            rot_g.append(i)
+            rot_r.append(g.param_refs[0])
+            rot_a.append(float(g.kind.alpha))
+            rot_d.append(len(drows))
+        elif name == "FixedUnitary" and len(targets) == 1:
+            m = np.asarray(g.kind.matrix, dtype=np.complex128)
+            axis = next((a for a, s in _PAULI_FIXED.items() if m.shape == (2, 2) and np.array_equal(m, s)), None)
+            if axis is not None:
+                form = N.FORM_PAULI
+                x, z, ny = pauli_masks("I" * targets[0] + axis)
+                rec["x_mask"], rec["z_mask"], rec["n_y"] = x, z, ny
+                fixed_p.append(i)
+        rec["form"] = form
+        if form == N.FORM_MAT:
+            mats.append(i)
+        for j in range(arity):
+            drows.append((i, g.param_refs[j], form))
+    derivs = np.zeros(len(drows), dtype=DERIV_DTYPE)
+    if drows:
+        d = np.asarray(drows, dtype=np.int64)
+        derivs["gate"], derivs["param_ref"], derivs["form"] = d[:, 0], d[:, 1], d[:, 2]
+    st = Structure(
+        arr, derivs, np.asarray(rot_g, dtype=np.int64), np.asarray(rot_r, dtype=np.int64),
+        np.asarray(rot_a, dtype=np.float64), np.asarray(rot_d, dtype=np.int64),
+        np.asarray(fixed_p, dtype=np.int64), mats, len(drows),
+    )
+    try:
+        ref = weakref.ref(circuit)
+    except TypeError:  # not weak-referenceable: do not cache
+        return st
+    if len(_cache) > 64:
+        _cache.clear()
+    _cache[id(circuit)] = (ref, st)
+    return st
+
+
+def _put(block: np.ndarray, m: np.ndarray) -> None:
+    flat = np.asarray(m, dtype=np.complex128).reshape(-1)
+    block[:] = 0
+    block[: flat.size] = flat
+
+
+def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Gate and derivative tables for one theta (raises NonInvertibleGateError)."""
+    st = _structure(circuit)
+    gates = st.gates.copy()
+    derivs = st.derivs.copy()
+    scale = derivative_scale()
+    if st.rot_gates.size:
+        ang = st.rot_alpha * params[st.rot_refs]
+        a = np.cos(ang) + 0j
+        b = 1j * np.sin(ang)
+        gates["fwd"][st.rot_gates, 0] = a
+        gates["fwd"][st.rot_gates, 1] = b
+        gates["rewind"][st.rot_gates, 0] = np.conj(a)
+        gates["rewind"][st.rot_gates, 1] = np.conj(b)
+        gates["adjoint"][st.rot_gates, 0] = np.conj(a)
+        gates["adjoint"][st.rot_gates, 1] = np.conj(b)
+        coef = (st.rot_alpha * 1j) * scale
+        derivs["k"][st.rot_derivs, 0] = coef * b
+        derivs["k"][st.rot_derivs, 1] = coef * a
+    if st.fixed_pauli.size:
+        for field in ("fwd", "rewind", "adjoint"):
+            gates[field][st.fixed_pauli, 1] = 1.0
+    if st.mat_gates:
+        first = np.concatenate([[0], np.cumsum(gates["nderiv"])])
+        for i in st.mat_gates:
+            g = circuit.gates[i]
+            name = kind_name(g)
+            m = bound_matrix(g, params)
+            adj = m.conj().T
+            if name == "NonUnitary":
+                try:
+                    rew = invert_small(m)
+                except ValueError as exc:
+                    raise NonInvertibleGateError(f"non-invertible gate {i}: {exc}") from exc
+            else:
+                rew = adj
+            _put(gates["fwd"][i], m)
+            _put(gates["rewind"][i], rew)
+            _put(gates["adjoint"][i], adj)
+            for j in range(len(g.param_refs)):
+                if name == "Phase":
+                    theta = float(params[g.param_refs[0]])
+                    k = np.diag([0.0, 1j * np.exp(1j * theta)])
+                else:
+                    k = matrix_derivative(g, params, j)
+                _put(derivs["k"][first[i] + j], k * scale)
+    return gates, derivs
+
+
+def lower_terms(obs) -> np.ndarray:
+    strings = pauli_strings(obs)
+    terms = np.zeros(len(strings), dtype=TERM_DTYPE)
+    for i, s in enumerate(strings):
+        terms[i] = (s.coeff, s.x_mask, s.z_mask, s.n_y, 0)
+    return terms
+
+
+class Problem:
+    """Owns the numpy tables and the svg_problem that points into them."""
+
+    def __init__(self, circuit, params, obs, input_state, with_derivs: bool = True):
+        self.gates, self.derivs = bind(circuit, params)
+        self.terms = lower_terms(obs)
+        self.num_derivs = len(self.derivs)
+        from .state import basis_index_of
+
+        basis = basis_index_of(input_state)
+        self.amps = None
+        if basis is None:
+            self.amps = np.ascontiguousarray(input_state.amplitudes, dtype=np.complex128)
+        p = N.svg_problem()
+        p.num_qubits = circuit.num_qubits
+        p.num_params = circuit.num_params
+        p.num_gates = len(self.gates)
+        p.num_derivs = self.num_derivs
+        p.num_terms = len(self.terms)
+        p.gates = self.gates.ctypes.data_as(C.POINTER(N.svg_gate))
+        p.derivs = self.derivs.ctypes.data_as(C.POINTER(N.svg_deriv))
+        p.terms = self.terms.ctypes.data_as(C.POINTER(N.svg_pauli_term))
+        p.input_basis = 0 if basis is None else basis
+        p.input_amps = None if self.amps is None else self.amps.ctypes.data
+        self.c = p
+
+    @property
+    def h2d_state_bytes(self) -> int:
+        return 0 if self.amps is None else self.amps.nbytes
