@@ -158,6 +158,13 @@ int svg_reverse_sweep(svg_engine* e, const svg_problem* p, svg_c128* sums_out,
  * svgrad/observable.py:114-116). derivs are ignored. */
 int svg_expectation(svg_engine* e, const svg_problem* p, svg_c128* energy_out, svg_stats* stats);
 
+/* Host-only planner introspection (no CUDA calls): the gate application
+ * order grouped into HBM passes.  order_out[G], pass_start_out[G+1],
+ * qmask_out[G] (tile qubits of each pass); sms = SM count to plan for (0: 148). */
+int svg_plan_inspect(const svg_problem* p, int tile_qubits, int sms, int32_t* order_out,
+                     int32_t* pass_start_out, uint64_t* qmask_out, int32_t* npasses_out,
+                     int32_t* tile_qubits_out);
+
 #ifdef __cplusplus
 }
 #endif

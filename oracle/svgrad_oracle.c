@@ -71,21 +71,43 @@ typedef struct {
 static const cplx PAULI[4][4] = {
     {1, 0, 0, 1}, {0, 1, 1, 0}, {0, -I, I, 0}, {1, 0, 0, -1}};
 
+static int cmp_int(const void* a, const void* b) { return *(const int*)a - *(const int*)b; }
+
+/* Enumerate exactly the groups the reference's _group_indices table holds:
+ * target bits 0, control bits 1, every other bit free (group id with zero
+ * bits inserted at the sorted fixed positions). */
 static void apply_matrix(cplx* amps, int n, const cplx* m, int nt, const int32_t* targets,
                          int nc, const int32_t* controls) {
-  const int64_t dim = (int64_t)1 << n;
-  int64_t tmask = 0, cmask = 0;
-  for (int k = 0; k < nt; ++k) tmask |= (int64_t)1 << targets[k];
-  for (int k = 0; k < nc; ++k) cmask |= (int64_t)1 << controls[k];
+  int64_t cmask = 0;
+  int fixed[64];
+  int nf = 0;
+  for (int k = 0; k < nt; ++k) fixed[nf++] = targets[k];
+  for (int k = 0; k < nc; ++k) {
+    fixed[nf++] = controls[k];
+    cmask |= (int64_t)1 << controls[k];
+  }
+  qsort(fixed, nf, sizeof(int), cmp_int);
   int64_t off[4] = {0, 0, 0, 0};
   for (int k = 0; k < nt; ++k) {
     const int64_t half = (int64_t)1 << k;
     for (int64_t s = 0; s < half; ++s) off[half + s] = off[s] + ((int64_t)1 << targets[k]);
   }
   const int g = 1 << nt;
+  const int64_t groups = (int64_t)1 << (n - nf);
 #pragma omp parallel for schedule(static)
-  for (int64_t idx = 0; idx < dim; ++idx) {
-    if ((idx & tmask) != 0 || (idx & cmask) != cmask) continue;
+  for (int64_t gi = 0; gi < groups; ++gi) {
+    int64_t idx = gi;
+    for (int f = 0; f < nf; ++f) {
+      const int64_t low = idx & (((int64_t)1 << fixed[f]) - 1);
+      idx = ((idx >> fixed[f]) << (fixed[f] + 1)) | low;
+    }
+    idx |= cmask;
+    if (g == 2) {
+      const cplx v0 = amps[idx], v1 = amps[idx + off[1]];
+      amps[idx] = m[0] * v0 + m[1] * v1;
+      amps[idx + off[1]] = m[2] * v0 + m[3] * v1;
+      continue;
+    }
     cplx v[4], w[4];
     for (int s = 0; s < g; ++s) v[s] = amps[idx + off[s]];
     for (int r = 0; r < g; ++r) {

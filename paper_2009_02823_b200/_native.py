@@ -19,7 +19,7 @@ FORM_PAULI, FORM_MAT = 0, 1
 EXPORTED = (
     "svg_abi_version", "svg_last_error", "svg_device_count", "svg_engine_create",
     "svg_engine_destroy", "svg_engine_set_stream", "svg_engine_set_option",
-    "svg_reverse_sweep", "svg_expectation",
+    "svg_reverse_sweep", "svg_expectation", "svg_plan_inspect",
 )
 
 
@@ -108,6 +108,10 @@ def load(path: str = LIB_PATH):
             C.POINTER(c128), C.POINTER(svg_stats),
         ]
         lib.svg_expectation.argtypes = [C.c_void_p, C.POINTER(svg_problem), C.POINTER(c128), C.POINTER(svg_stats)]
+        lib.svg_plan_inspect.argtypes = [
+            C.POINTER(svg_problem), C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+        ]
         for name in EXPORTED:
             getattr(lib, name).restype = C.c_char_p if name == "svg_last_error" else C.c_int
         if lib.svg_abi_version() != ABI_VERSION:
@@ -179,6 +183,22 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+def plan_inspect(problem: svg_problem, tile_qubits: int = 0, sms: int = 0):
+    """Planner output without a GPU: (order, pass_start, qmasks, tile_qubits)."""
+    import numpy as np
+
+    lib = load()
+    G = max(1, problem.num_gates)
+    order = np.zeros(G, dtype=np.int32)
+    start = np.zeros(G + 1, dtype=np.int32)
+    qmask = np.zeros(G, dtype=np.uint64)
+    npasses, k = C.c_int32(), C.c_int32()
+    check(lib.svg_plan_inspect(C.byref(problem), int(tile_qubits), int(sms), order.ctypes.data,
+                               start.ctypes.data, qmask.ctypes.data, C.byref(npasses), C.byref(k)))
+    m = npasses.value
+    return order[: problem.num_gates], start[: m + 1], qmask[:m], k.value
 
 
 _engines: dict[int, Engine] = {}

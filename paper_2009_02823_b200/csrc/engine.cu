@@ -605,4 +605,35 @@ int svg_expectation(svg_engine* e, const svg_problem* p, svg_c128* energy_out, s
   return run(e, p, false, nullptr, nullptr, energy_out, stats);
 }
 
+int svg_plan_inspect(const svg_problem* p, int tile_qubits, int sms, int32_t* order_out,
+                     int32_t* pass_start_out, uint64_t* qmask_out, int32_t* npasses_out,
+                     int32_t* tile_qubits_out) {
+  try {
+    validate(p);
+    const int n = p->num_qubits;
+    PlanParams pp;
+    pp.n = n;
+    pp.k = choose_tile_qubits(n, tile_qubits, sms > 0 ? sms : 148);
+    pp.b = (n <= pp.k) ? n : std::min(5, pp.k - 2);
+    std::vector<GateShape> shapes(p->num_gates);
+    for (int i = 0; i < p->num_gates; ++i) shapes[i] = gate_shape(p->gates[i]);
+    const std::vector<Pass> passes = plan_gate_passes(shapes, pp);
+    int pos = 0;
+    for (size_t j = 0; j < passes.size(); ++j) {
+      if (pass_start_out) pass_start_out[j] = pos;
+      if (qmask_out) qmask_out[j] = passes[j].qmask;
+      for (int g : passes[j].items) {
+        if (order_out) order_out[pos] = g;
+        ++pos;
+      }
+    }
+    if (pass_start_out) pass_start_out[passes.size()] = pos;
+    if (npasses_out) *npasses_out = static_cast<int32_t>(passes.size());
+    if (tile_qubits_out) *tile_qubits_out = pp.k;
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_EINVAL, ex.what());
+  }
+}
+
 }  // extern "C"

@@ -92,6 +92,7 @@ std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, cons
 
 int choose_tile_qubits(int n, int requested, int sms) {
   if (requested > 0) return std::min(requested, n);
+  if (n <= 10) return n;  // whole state in one tile: one CTA, no HBM round trips between passes
   int k = std::min(n, 10);
   // keep at least ~4 tiles per SM so the persistent grid stays balanced
   while (k > 7 && (n - k) < 62 && (1ll << (n - k)) < 4ll * sms) --k;

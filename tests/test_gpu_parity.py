@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path through the drop-in API vs the reference's golden outputs and the oracle.
+
+Bar (BASELINE.json north_star): every gradient entry within 1e-10 abs-or-rel,
+energy within 1e-12; exact OpCounters.  Everything here runs through
+``paper_2009_02823_b200.reverse_mode_gradient`` -> libsvgb200.so (C-ABI).
+"""
+import numpy as np
+import pytest
+
+import paper_2009_02823_b200 as sv
+from cases import config_cases, large_config_cases, small_cases
+from conftest import cvec, load_golden, materialize, max_err
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = 1e-10
+ENERGY_TOL = 1e-12
+
+GOLD = load_golden()
+SMALL = {**small_cases(), **config_cases()}
+
+
+def _run(circ, theta, obs, inp, method):
+    if method == "non_hermitian":
+        return sv.non_hermitian_gradient(circ, theta, obs, inp)
+    return sv.reverse_mode_gradient(circ, theta, obs, inp)
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_gpu_matches_reference_golden(name):
+    rec = GOLD[name]
+    circ, theta, obs, inp, method = materialize(SMALL[name])
+    rep = _run(circ, theta, obs, inp, method)
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+    assert vars(rep.counters) == rec["counters"]
+    if method == "reverse":
+        assert np.all(rep.values.imag == 0.0)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3_n20", "cfg4_n20", "cfg5_n20", "cfg3"])
+def test_gpu_matches_reference_golden_large(name):
+    gold = load_golden(f"golden_{name}.json")[name]
+    circ, theta, obs, inp, method = materialize(large_config_cases()[name])
+    rep = _run(circ, theta, obs, inp, method)
+    err = max_err(rep.values, cvec(gold["values"]))
+    assert err <= GRAD_TOL, err
+    assert abs(rep.energy - complex(*gold["energy"])) <= ENERGY_TOL
+    assert vars(rep.counters) == gold["counters"]
+
+
+@pytest.mark.parametrize("tile", [0, 7, 8, 9, 11, 12])
+def test_tile_size_invariance(tile):
+    """Different pass plans (tile widths) reorder commuting gates only."""
+    circ, theta, obs, inp, _ = materialize(SMALL["cfg5_n15"])
+    eng = sv._native.engine()
+    eng.set_option("tile_qubits", tile)
+    try:
+        rep = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    finally:
+        eng.set_option("tile_qubits", 0)
+    rec = GOLD["cfg5_n15"]
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+
+
+def test_pass_cap_invariance():
+    circ, theta, obs, inp, _ = materialize(SMALL["cfg3_n14"])
+    eng = sv._native.engine()
+    ref = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    eng.set_option("max_gates_per_pass", 3)
+    try:
+        rep = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    finally:
+        eng.set_option("max_gates_per_pass", 0)
+    assert max_err(rep.values, ref.values) <= 1e-12
+
+
+def test_bitwise_deterministic():
+    circ, theta, obs, inp, _ = materialize(SMALL["cfg4_n16"])
+    a = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    b = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    assert np.array_equal(a.values, b.values) and a.energy == b.energy
+
+
+def test_basis_fast_path_equals_dense_input():
+    circ, theta, obs, _, _ = materialize(SMALL["cfg2_n12"])
+    dense = sv.reverse_mode_gradient(circ, theta, obs, sv.init_basis_state(12, 5))
+    fast = sv.reverse_mode_gradient(circ, theta, obs, sv.BasisState(12, 5))
+    assert max_err(fast.values, dense.values) <= 1e-13
+
+
+def test_accepts_reference_style_objects_via_duck_typing():
+    """Inputs are duck-typed: a foreign Circuit/Observable/StateVector works."""
+    from types import SimpleNamespace as NS
+
+    circ, theta, obs, inp, _ = materialize(SMALL["family_B4_0"])
+    foreign_gates = tuple(NS(kind=g.kind, targets=g.targets, controls=g.controls, param_refs=g.param_refs)
+                          for g in circ.gates)
+    fc = NS(num_qubits=circ.num_qubits, gates=foreign_gates, num_params=circ.num_params)
+    fo = NS(num_qubits=obs.num_qubits, terms=obs.terms, is_hermitian=True)
+    fs = NS(num_qubits=inp.num_qubits, amplitudes=inp.amplitudes)
+    rep = sv.reverse_mode_gradient(fc, theta, fo, fs)
+    assert max_err(rep.values, cvec(GOLD["family_B4_0"]["values"])) <= GRAD_TOL
+
+
+def test_errors_match_reference():
+    z1 = sv.Observable(1, ((1.0, "Z"),))
+    circ = sv.Circuit(1, (sv.ry(0, 0),), 1)
+    with pytest.raises(ValueError, match="non_hermitian_gradient"):
+        sv.reverse_mode_gradient(circ, [0.1], sv.Observable(1, ((1.0, "+"),)), sv.init_basis_state(1))
+    with pytest.raises(ValueError):
+        sv.reverse_mode_gradient(circ, [0.1, 0.2], z1, sv.init_basis_state(1))
+    with pytest.raises(ValueError):
+        sv.reverse_mode_gradient(circ, [0.1], sv.builtin_observable("z_all", 2), sv.init_basis_state(1))
+    bad = sv.Gate(sv.NonUnitary(lambda t: np.zeros((2, 2)), 1), (0,), (), (0,))
+    with pytest.raises(sv.NonInvertibleGateError, match="gate 1"):
+        sv.reverse_mode_gradient(sv.Circuit(1, (sv.ry(0, 0), bad), 1), [0.1], z1, sv.init_basis_state(1))
+
+
+def test_live_state_audit_peak():
+    audit = sv.LiveStateAudit()
+    circ = sv.Circuit(2, tuple(sv.rx(i % 2, i) for i in range(10)), 10)
+    sv.reverse_mode_gradient(circ, np.zeros(10), sv.builtin_observable("z_all", 2), sv.init_basis_state(2), audit=audit)
+    assert audit.peak == 4 and audit.live == 0
+
+
+def test_negative_control_is_detected():
+    circ, theta, obs, inp, _ = materialize(SMALL["family_D4_0"])
+    with sv.perturbed_derivative_scale(1.01):
+        rep = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    assert max_err(rep.values, cvec(GOLD["family_D4_0"]["values"])) > 1e-4
+
+
+def test_expectation_matches_oracle():
+    from oracle import oracle
+
+    circ, theta, obs, inp, _ = materialize(SMALL["all_kinds_6_random"])
+    e = sv.circuit_expectation(circ, theta, obs, inp)
+    assert abs(e - oracle.expectation(circ, theta, obs, inp.amplitudes)) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 22), (5, 21)])
+def test_gpu_matches_oracle_midsize(cfg, n):
+    """Sizes between the fixtures: the pinned C oracle is the checker."""
+    from oracle import oracle
+
+    w = sv.build_workload(cfg, n)
+    inp = sv.init_basis_state(n)
+    rep = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp)
+    vals, energy, counters = oracle.reverse_mode_values(w.circuit, w.theta, w.observable, inp.amplitudes)
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
+    assert vars(rep.counters) == counters
+
+
+def _parameter_shift(w, k):
+    """Exact for alpha=-1/2 Pauli rotations: g_k = [E(t+pi/2) - E(t-pi/2)] / 2."""
+    inp = sv.BasisState(w.num_qubits)
+    tp, tm = w.theta.copy(), w.theta.copy()
+    tp[k] += np.pi / 2
+    tm[k] -= np.pi / 2
+    ep = sv.circuit_expectation(w.circuit, tp, w.observable, inp)
+    em = sv.circuit_expectation(w.circuit, tm, w.observable, inp)
+    return ((ep - em) / 2).real
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_parameter_shift(cfg):
+    """Full BASELINE sizes (cfg3 n=26, cfg4 n=30): size-independent parameter-shift identity."""
+    w = sv.build_workload(cfg)
+    rep = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, sv.BasisState(w.num_qubits))
+    for k in (0, w.circuit.num_params // 2, w.circuit.num_params - 1):
+        assert abs(rep.values[k].real - _parameter_shift(w, k)) <= 1e-9
+    e = sv.circuit_expectation(w.circuit, w.theta, w.observable, sv.BasisState(w.num_qubits))
+    assert abs(e - rep.energy) <= ENERGY_TOL

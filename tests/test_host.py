@@ -1,0 +1,115 @@
+"""CPU-only checks of the host side: C-ABI surface, table layouts, lowering, planner."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2009_02823_b200 as sv
+from cases import config_cases, small_cases
+from conftest import ROOT, cvec, gpu_available, load_golden, materialize, max_err
+from emulator import emulate
+from paper_2009_02823_b200 import _native, lowering
+
+GOLD = load_golden()
+CASES = {**small_cases(), **config_cases()}
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "svgrad_b200.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(svg_\w+)\(", header, flags=re.M))
+    assert declared == set(_native.EXPORTED)
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert _native.load().svg_abi_version() == _native.ABI_VERSION
+
+
+@pytest.mark.parametrize("dtype,ctype", [
+    (lowering.GATE_DTYPE, _native.svg_gate),
+    (lowering.DERIV_DTYPE, _native.svg_deriv),
+    (lowering.TERM_DTYPE, _native.svg_pauli_term),
+])
+def test_numpy_tables_match_c_layout(dtype, ctype):
+    assert dtype.itemsize == ctypes.sizeof(ctype)
+    for name, _ in ctype._fields_:
+        assert dtype.fields[name][1] == getattr(ctype, name).offset, name
+
+
+@pytest.mark.skipif(gpu_available(), reason="checks the no-GPU failure mode")
+def test_no_silent_cpu_fallback():
+    circ = sv.Circuit(1, (sv.ry(0, 0),), 1)
+    with pytest.raises(sv.NativeUnavailable):
+        sv.reverse_mode_gradient(circ, [0.3], sv.Observable(1, ((1.0, "Z"),)), sv.init_basis_state(1))
+
+
+EMULATED = [n for n in sorted(CASES) if GOLD[n]["num_qubits"] <= 12 and GOLD[n]["method"] == "reverse"]
+
+
+@pytest.mark.parametrize("name", EMULATED)
+def test_lowered_tables_reproduce_reference(name):
+    """Binding + generators + planner order + accumulation order, executed densely."""
+    rec = GOLD[name]
+    circ, theta, obs, inp, _ = materialize(CASES[name])
+    sums, energy, _ = emulate(circ, theta, obs, inp, tile_qubits=0)
+    assert max_err(2 * sums.real, cvec(rec["values"]).real) <= 1e-10
+    assert abs(energy - complex(*rec["energy"])) <= 1e-12
+
+
+@pytest.mark.parametrize("name,tile", [("cfg3_n14", 7), ("cfg5_n11", 7), ("cfg4_n12", 8), ("all_kinds_6_random", 7)])
+def test_planner_reordering_is_exact(name, tile):
+    rec = GOLD[name]
+    circ, theta, obs, inp, _ = materialize(CASES[name])
+    sums, energy, (order, start, qmasks, k) = emulate(circ, theta, obs, inp, tile_qubits=tile)
+    assert max_err(2 * sums.real, cvec(rec["values"]).real) <= 1e-10
+    assert sorted(order.tolist()) == list(range(len(circ.gates)))
+    prob = lowering.Problem(circ, theta, obs, inp)
+    for p in range(len(qmasks)):
+        q = int(qmasks[p])
+        assert bin(q).count("1") == min(k, circ.num_qubits)
+        for gi in order[start[p]: start[p + 1]]:
+            g = prob.gates[gi]
+            flip = int(g["x_mask"]) if g["form"] == _native.FORM_PAULI else sum(1 << t for t in g["targets"][: g["ntargets"]])
+            assert flip & ~q == 0
+
+
+def test_plan_fuses_full_size_configs():
+    """Pass counts at BASELINE sizes (host planning only, no allocation)."""
+    for cfg in (2, 3, 4, 5):
+        w = sv.build_workload(cfg)
+        prob = lowering.Problem(w.circuit, w.theta, w.observable, sv.BasisState(w.num_qubits))
+        order, start, qmasks, k = _native.plan_inspect(prob.c, 0, 148)
+        passes = len(start) - 1
+        assert passes < w.num_gates / 4, (cfg, passes)
+
+
+def test_pauli_lowering_of_rotations():
+    """a I + b P of the tables equals the reference closed form cos(at) I + i sin(at) P."""
+    from paper_2009_02823_b200.ir import bound_matrix, pauli_product
+
+    theta = np.array([0.37, -1.2])
+    circ = sv.Circuit(3, (sv.rp("XY", (0, 2), 0), sv.cry(1, 2, 1, alpha=0.8)), 2)
+    gates, derivs = lowering.bind(circ, theta)
+    for i, g in enumerate(circ.gates):
+        P = pauli_product(g.kind.axes)
+        U = gates[i]["fwd"][0] * np.eye(P.shape[0]) + gates[i]["fwd"][1] * P
+        assert np.allclose(U, bound_matrix(g, theta), atol=1e-15)
+        R = gates[i]["rewind"][0] * np.eye(P.shape[0]) + gates[i]["rewind"][1] * P
+        assert np.allclose(R @ U, np.eye(P.shape[0]), atol=1e-15)
+        K = derivs[i]["k"][0] * np.eye(P.shape[0]) + derivs[i]["k"][1] * P
+        # reference derivative action: sigma per axis, then the bound rotation, scalar alpha*i
+        assert np.allclose(K, g.kind.alpha * 1j * (U @ P), atol=1e-15)
+
+
+def test_non_pauli_observable_letters_expand_exactly():
+    from paper_2009_02823_b200.operators import dense_matrix, pauli_strings
+    from paper_2009_02823_b200.ir import pauli_product
+
+    obs = sv.Observable(3, ((0.7, "H+-"), (1.5j, "-ZH"), (-0.2, "IIY")))
+    dense = np.zeros((8, 8), dtype=complex)
+    for s in pauli_strings(obs):
+        letters = "".join("Y" if (s.x_mask >> q) & (s.z_mask >> q) & 1 else "X" if (s.x_mask >> q) & 1
+                          else "Z" if (s.z_mask >> q) & 1 else "I" for q in range(3))
+        dense += s.coeff * pauli_product(letters)
+    assert np.allclose(dense, dense_matrix(obs), atol=1e-15)
