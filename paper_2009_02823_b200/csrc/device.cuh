@@ -51,7 +51,7 @@ struct PassDesc {
   uint64_t rest;         // non-tile qubit mask (tile id bits are deposited here)
   int64_t part_off;      // this pass's slice of the partials buffer
   int32_t accumulate;    // observable pass: lambda += (1) or lambda = (0)
-  int32_t reserved;
+  int32_t untiled;       // observable pass over full-width masks (no tile)
   uint8_t q[kMaxQubits]; // tile qubits ascending
 };
 

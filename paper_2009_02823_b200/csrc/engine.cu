@@ -279,7 +279,13 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // observable passes (terms grouped by flip mask into tiles)
   std::vector<uint64_t> flips(p->num_terms);
   for (int t = 0; t < p->num_terms; ++t) flips[t] = p->terms[t].x_mask;
-  const std::vector<Pass> tpasses = plan_term_passes(flips, pp);
+  std::vector<int> direct;
+  std::vector<Pass> tpasses = plan_term_passes(flips, pp, &direct);
+  if (!direct.empty()) {  // wide flip masks: one untiled gather pass (qmask 0)
+    Pass ps;
+    ps.items = direct;
+    tpasses.push_back(ps);
+  }
   int64_t part = 0;
   const int64_t energy_off = 0;
   for (size_t j = 0; j < tpasses.size(); ++j) {
@@ -287,13 +293,20 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     const TileMap tm = tile_map(ps.qmask);
     Launch l{make_desc(n, L.k, ps.qmask), 0, 0};
     l.d.op_begin = static_cast<int>(L.terms.size());
+    l.d.untiled = ps.qmask == 0;
     for (int ti : ps.items) {
       const svg_pauli_term& src = p->terms[ti];
       DevTerm dt;
       dt.c = cm(d2(src.coeff), ipow(src.n_y));
-      dt.xl = tm.local(src.x_mask);
-      dt.zl = tm.local(src.z_mask);
-      dt.zo = src.z_mask & ~tm.qmask;
+      if (l.d.untiled) {  // full masks: x split over (xl, zl), z in zo
+        dt.xl = static_cast<uint32_t>(src.x_mask);
+        dt.zl = static_cast<uint32_t>(src.x_mask >> 32);
+        dt.zo = src.z_mask;
+      } else {
+        dt.xl = tm.local(src.x_mask);
+        dt.zl = tm.local(src.z_mask);
+        dt.zo = src.z_mask & ~tm.qmask;
+      }
       L.terms.push_back(dt);
     }
     l.d.op_end = static_cast<int>(L.terms.size());
@@ -340,8 +353,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     l.grid = grid_for(0, l.smem);
   }
   for (Launch& l : L.obs) {
-    l.smem = obs_smem(L.k, l.d.b);
-    l.grid = grid_for(1, l.smem);
+    l.smem = l.d.untiled ? 0 : obs_smem(L.k, l.d.b);
+    l.grid = l.d.untiled ? std::max(1, std::min<int>(e->sms * 8, static_cast<int>(std::min<int64_t>(
+                               int64_t(1) << std::max(0, n - 8), 1 << 30))))
+                         : grid_for(1, l.smem);
     l.d.part_off = part;
     part += l.grid;
   }
@@ -444,7 +459,12 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     CK(cudaEventRecord(e->ev[1], s));
     for (const Launch& l : L.fwd) launch_fwd(l.d, l.grid, l.smem, s, psi, dops, dcoef);
     CK(cudaEventRecord(e->ev[2], s));
-    for (const Launch& l : L.obs) launch_obs(l.d, l.grid, l.smem, s, psi, lam, dterms, part);
+    for (const Launch& l : L.obs) {
+      if (l.d.untiled)
+        launch_obs_direct(l.d, l.grid, s, psi, lam, dterms, part);
+      else
+        launch_obs(l.d, l.grid, l.smem, s, psi, lam, dterms, part);
+    }
     CK(cudaEventRecord(e->ev[3], s));
     for (const Launch& l : L.rev) launch_rev(l.d, l.grid, l.smem, s, psi, lam, dops, dcoef, part);
     CK(cudaEventRecord(e->ev[4], s));

@@ -256,6 +256,40 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
   }
 }
 
+// Untiled observable pass for flip masks too wide for a tile: plain gathers.
+__global__ void __launch_bounds__(kThreads) k_obs_direct(const double2* __restrict__ psi,
+                                                         double2* __restrict__ lam, PassDesc d,
+                                                         const DevTerm* __restrict__ terms,
+                                                         double2* __restrict__ partials) {
+  __shared__ double2 wsum[kWarps];
+  double2 e = make_double2(0.0, 0.0);
+  const uint64_t dim = 1ull << d.n;
+  for (uint64_t m = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; m < dim; m += uint64_t(gridDim.x) * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = d.op_begin; j < d.op_end; ++j) {
+      const DevTerm tm = terms[j];
+      const uint64_t x = uint64_t(tm.xl) | (uint64_t(tm.zl) << 32);
+      const uint64_t src = m ^ x;
+      acc = cfma(cneg_if(tm.c, par64(src & tm.zo)), psi[src], acc);
+    }
+    if (d.accumulate) {
+      const double2 old = lam[m];
+      lam[m] = make_double2(old.x + acc.x, old.y + acc.y);
+    } else {
+      lam[m] = acc;
+    }
+    e = cjfma(psi[m], acc, e);
+  }
+  e = warp_sum(e);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int w = 0; w < kWarps; ++w) s = make_double2(s.x + wsum[w].x, s.y + wsum[w].y);
+    partials[d.part_off + blockIdx.x] = s;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_rev_pass(double2* __restrict__ phi,
                                                        double2* __restrict__ lam, PassDesc d,
                                                        const DevOp* __restrict__ ops,
@@ -363,6 +397,10 @@ void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double
 void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi,
                 double2* lam, const DevTerm* terms, double2* partials) {
   k_obs_pass<<<grid, kThreads, smem, s>>>(psi, lam, d, terms, partials);
+}
+void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, double2* lam,
+                       const DevTerm* terms, double2* partials) {
+  k_obs_direct<<<grid, kThreads, 0, s>>>(psi, lam, d, terms, partials);
 }
 void launch_rev(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* phi, double2* lam,
                 const DevOp* ops, const double2* coef, double2* partials) {

@@ -18,6 +18,8 @@ void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double
                 const DevOp* ops, const double2* coef);
 void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi,
                 double2* lam, const DevTerm* terms, double2* partials);
+void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, double2* lam,
+                       const DevTerm* terms, double2* partials);
 void launch_rev(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* phi, double2* lam,
                 const DevOp* ops, const double2* coef, double2* partials);
 void launch_finalize(const double2* partials, const SumSpec* specs, int count, double2* out,

@@ -65,12 +65,16 @@ std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const P
   return passes;
 }
 
-std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp) {
+std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp,
+                                   std::vector<int>* direct) {
   std::vector<Pass> passes;
   std::vector<uint64_t> masks;  // unpadded tile sets
   for (int t = 0; t < static_cast<int>(term_flips.size()); ++t) {
     const uint64_t f = term_flips[t];
-    if (popc(low_mask(pp.b) | f) > pp.k) throw std::runtime_error("observable term flips more qubits than a tile holds");
+    if (popc(low_mask(pp.b) | f) > pp.k) {  // too wide for a tile: untiled gather pass
+      direct->push_back(t);
+      continue;
+    }
     int chosen = -1;
     for (int j = 0; j < static_cast<int>(passes.size()); ++j) {
       if (popc(masks[j] | f) <= pp.k && static_cast<int>(passes[j].items.size()) < pp.max_items) {
@@ -95,7 +99,7 @@ int choose_tile_qubits(int n, int requested, int sms) {
   if (n <= 10) return n;  // whole state in one tile: one CTA, no HBM round trips between passes
   int k = std::min(n, 10);
   // keep at least ~4 tiles per SM so the persistent grid stays balanced
-  while (k > 7 && (n - k) < 62 && (1ll << (n - k)) < 4ll * sms) --k;
+  while (k > 9 && (n - k) < 62 && (1ll << (n - k)) < 4ll * sms) --k;
   return std::min(k, n);
 }
 

@@ -49,7 +49,10 @@ GateShape gate_shape(const svg_gate& g);
 std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp);
 
 // Observable passes: terms grouped so each pass's flip masks fit one tile.
-std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp);
+// Terms whose flip mask cannot share a tile with the low qubits go to `direct`
+// (handled by an untiled gather kernel).
+std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp,
+                                   std::vector<int>* direct);
 
 // Tile size choice for n qubits on `sms` SMs (auto when requested == 0).
 int choose_tile_qubits(int n, int requested, int sms);

@@ -140,6 +140,21 @@ def test_expectation_matches_oracle():
     assert abs(e - oracle.expectation(circ, theta, obs, inp.amplitudes)) <= ENERGY_TOL
 
 
+@pytest.mark.parametrize("n", [11, 13])
+def test_wide_flip_terms_use_untiled_pass(n):
+    """hadamard_all expands into Pauli strings flipping up to n qubits (> tile width)."""
+    from oracle import oracle
+
+    circ = sv.Circuit(n, tuple(sv.ry(q, q) for q in range(n)) + tuple(sv.cx(q, (q + 1) % n) for q in range(n)), n)
+    theta = np.linspace(0.1, 2.9, n)
+    obs = sv.builtin_observable("hadamard_all", n)
+    inp = sv.init_basis_state(n)
+    rep = sv.reverse_mode_gradient(circ, theta, obs, inp)
+    vals, energy, _ = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
 @pytest.mark.parametrize("cfg,n", [(3, 22), (5, 21)])
 def test_gpu_matches_oracle_midsize(cfg, n):
     """Sizes between the fixtures: the pinned C oracle is the checker."""
