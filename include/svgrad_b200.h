@@ -87,7 +87,9 @@ typedef struct {
   int32_t gate;
   int32_t param_ref;
   int32_t form;
-  int32_t reserved;
+  int32_t basis;        /* 0: K acts on phi_i (before gate i, the reference's probe order);
+                           1: K acts on phi_{i+1} (after gate i); the engine converts via
+                           K_post = K_pre * U^-1 / K_pre = K_post * U */
   svg_c128 k[16];
 } svg_deriv;
 
@@ -101,13 +103,16 @@ typedef struct {
   int32_t reserved;
 } svg_pauli_term;
 
+/* svg_problem.flags */
+#define SVG_FLAG_REAL_SUMS 1  /* only Re(sums) is needed (Hermitian 2*Re path); imag may be 0 */
+
 typedef struct {
   int32_t num_qubits;
   int32_t num_params;
   int32_t num_gates;
   int32_t num_derivs;        /* = sum of arities, gate-major order */
   int32_t num_terms;
-  int32_t flags;             /* reserved, 0 */
+  int32_t flags;             /* SVG_FLAG_* */
   const svg_gate* gates;
   const svg_deriv* derivs;
   const svg_pauli_term* terms;
@@ -142,7 +147,7 @@ int svg_engine_destroy(svg_engine* e);
 /* Launch on an external cudaStream_t (passed as void*); NULL = engine's own stream. */
 int svg_engine_set_stream(svg_engine* e, void* stream);
 /* Options: "tile_qubits" (0 = auto), "profile" (1 = per-phase CUDA-event times in svg_stats),
-   "max_gates_per_pass" (0 = auto). */
+   "max_gates_per_pass" (0 = auto), "kernel" (0 auto, 1 shared-memory tiles, 2 register tiles). */
 int svg_engine_set_option(svg_engine* e, const char* key, int64_t value);
 
 /* The hot path: one full adjoint sweep.  sums_out[num_params] receives the

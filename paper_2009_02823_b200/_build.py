@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsvgb200.so")
-SOURCES = ["engine.cu", "kernels.cu", "plan.cpp"]
+SOURCES = ["engine.cu", "kernels.cu", "kernels_reg.cu", "plan.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

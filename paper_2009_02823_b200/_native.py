@@ -46,7 +46,7 @@ class svg_gate(C.Structure):
 class svg_deriv(C.Structure):
     _fields_ = [
         ("gate", C.c_int32), ("param_ref", C.c_int32), ("form", C.c_int32),
-        ("reserved", C.c_int32), ("k", C128x16),
+        ("basis", C.c_int32), ("k", C128x16),
     ]
 
 

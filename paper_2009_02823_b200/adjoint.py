@@ -87,9 +87,14 @@ def _account(counters, audit, num_gates: int, num_derivs: int) -> None:
     audit.release()
 
 
-def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, stats: dict | None = None):
-    """Equivalent of the reference's ``_reverse_sweep``: (complex sums[P], energy)."""
-    problem = Problem(circuit, params, obs, input_state)
+def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, stats: dict | None = None,
+          real_sums: bool = False):
+    """Equivalent of the reference's ``_reverse_sweep``: (complex sums[P], energy).
+
+    ``real_sums=True`` lets the engine skip Im(sums) (returned as 0) when the
+    caller only forms 2*Re, as the Hermitian path does (svgrad/gradients.py:198).
+    """
+    problem = Problem(circuit, params, obs, input_state, real_sums=real_sums)
     sums, _, energy, st = _native.engine(device).reverse_sweep(problem.c, circuit.num_params, problem.num_derivs)
     _account(counters, audit, len(circuit.gates), problem.num_derivs)
     out = np.ctypeslib.as_array(sums).view(np.complex128)[: circuit.num_params].copy()
@@ -105,7 +110,8 @@ def reverse_mode_gradient(circuit, params, obs, input_state, audit: LiveStateAud
         raise ValueError(_HERMITIAN_MSG)
     params = _check_call(circuit, params, obs, input_state)
     counters = OpCounters()
-    sums, energy = sweep(circuit, params, obs, input_state, counters, audit or LiveStateAudit(), device, stats)
+    sums, energy = sweep(circuit, params, obs, input_state, counters, audit or LiveStateAudit(), device, stats,
+                         real_sums=True)
     return GradientReport((2.0 * sums.real).astype(complex), energy, counters)
 
 

@@ -8,6 +8,7 @@ namespace svgb {
 constexpr int kMaxQubits = 40;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kRegBits = 4;  // amplitudes per thread per buffer = 2^kRegBits (register-tile passes)
 
 enum OpKind : uint32_t {
   OP_APPLY_PAULI = 0,  // buf <- a*buf + b'*Psign buf          (b' = b * i^{n_y})
@@ -52,8 +53,58 @@ struct PassDesc {
   int64_t part_off;      // this pass's slice of the partials buffer
   int32_t accumulate;    // observable pass: lambda += (1) or lambda = (0)
   int32_t untiled;       // observable pass over full-width masks (no tile)
+  int32_t seg_begin, seg_end;  // register-tile passes: segment range
+  int32_t smem_tiles;    // register-tile passes: 1 if the pass stages tiles in shared memory
+  int32_t pad0;
   uint8_t q[kMaxQubits]; // tile qubits ascending
 };
+
+// ---- register-tile passes (kernels_reg.cu) ----
+//
+// A register-tile pass keeps each thread's share of the tile in registers:
+// thread (warp w, lane l) holds 2^R amplitudes per buffer whose
+// SEGMENT-LOCAL index is  t = l | j << 5 | w << (5 + R)  (j = register slot).
+// Lane bits are always tile positions 0..4 (global qubits 0..4, so global
+// loads/stores are 512-byte coalesced rows); each segment chooses which tile
+// positions are register bits and which are warp bits.  Gates may flip lane
+// bits (warp shuffles) and register bits (register permutations) but never
+// warp bits; between segments the tile is transposed through shared memory.
+
+enum RegOpKind : uint32_t {
+  ROP_FWD = 0,  // psi <- a psi + b' Psign psi                                   (forward)
+  ROP_REV = 1,  // [slot += <lam| K' |phi>]; phi <- a phi + b' Psign phi          (reverse, rewind)
+  ROP_LAM = 2,  // lam <- a lam + b' Psign lam                                    (reverse, adjoint)
+};
+enum RegOpFlags : uint32_t {
+  RF_IP = 1u,       // ROP_REV accumulates the generator term before rewinding
+  RF_IP_RE = 2u,    // accumulate Re(z)
+  RF_IP_IM = 4u,    // accumulate Im(z)
+  RF_IP_DIAG = 8u,  // K' has an identity part ka: also accumulate z2 = sum conj(lam) phi
+  RF_ROT = 16u,     // a is real and b' is real (or imaginary with RF_BI): 4-flop update
+  RF_BI = 32u,      // b' is imaginary: multiply the partner by i and use b'.y
+};
+
+struct RegOp {
+  uint32_t kind, flags;
+  uint32_t x, z, c;  // segment-local flip / sign / control masks
+  uint32_t slot;
+  uint64_t pad;
+  uint64_t zo, co;   // non-tile (global) sign / control masks
+  double2 a, b;      // operator a I + b' Psign  (b' includes i^{n_y})
+  double2 ka, kb;    // generator ka I + kb' Psign, relative to the post-gate state
+};
+static_assert(sizeof(RegOp) == 112, "RegOp layout");
+
+enum SegKind : int32_t { SEG_REG = 0, SEG_SMEM = 1 };
+
+struct SegDesc {
+  int32_t kind;
+  int32_t op_begin, op_end;  // RegOps (SEG_REG) or DevOps (SEG_SMEM)
+  int32_t same_map;          // SEG_REG: identical layout to the previous register segment
+  uint8_t regpos[8];         // tile positions of register bits
+  uint8_t warppos[8];        // tile positions of warp bits
+};
+static_assert(sizeof(SegDesc) == 32, "SegDesc layout");
 
 // Entry of the finalize map: deterministic sum of `count` partials at `off`.
 struct SumSpec {

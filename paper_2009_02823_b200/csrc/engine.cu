@@ -105,22 +105,39 @@ struct HostBuf {
   }
 };
 
+enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG };
+
 struct Launch {
   PassDesc d;
-  int grid;
-  size_t smem;
+  int grid = 0;
+  size_t smem = 0;
+  int kind = L_SMEM_FWD;
+  int nb = 1;       // L_REG: buffers in the pass (1 forward, 2 reverse)
+  int threads = kThreads;
+  bool tiles = false;  // L_REG: stages the tile through shared memory
 };
 
 // Everything a sweep needs on the host side, built from one svg_problem.
 struct Lowered {
   int n = 0, k = 0, b = 0;
+  bool reg = false;  // register-tile kernels in use
   std::vector<DevOp> ops;
   std::vector<double2> coef;
   std::vector<DevTerm> terms;
+  std::vector<RegOp> rops;
+  std::vector<SegDesc> segs;
   std::vector<SumSpec> sums;  // [num_derivs] derivative terms, then [1] energy
   std::vector<Launch> fwd, obs, rev;
   int64_t partial_count = 0;
   int64_t pass_bytes = 0;
+};
+
+// Derivative generator in both bases: `pre` acts on the state before the
+// gate (the ABI's basis 0, the reference's probe order), `post` on the state
+// after it (basis 1; what the register kernels fuse with the rewind).
+struct Gen {
+  svg_c128 pre[16];
+  svg_c128 post[16];
 };
 
 }  // namespace
@@ -131,7 +148,7 @@ struct svg_engine {
   size_t max_smem = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0;
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0;
   DeviceBuf psi, lam, partials, blob, results;
   HostBuf hblob, hres;
   cudaEvent_t ev[6] = {};
@@ -170,6 +187,7 @@ void validate(const svg_problem* p) {
       if (dv.gate != i) throw InvalidArg("derivative table not gate-major");
       if (dv.param_ref < 0 || dv.param_ref >= p->num_params) throw InvalidArg("param_ref out of range");
       if (dv.form != g.form) throw InvalidArg("derivative form differs from its gate's form");
+      if (dv.basis != 0 && dv.basis != 1) throw InvalidArg("derivative basis must be 0 or 1");
     }
   }
   if (d != p->num_derivs) throw InvalidArg("derivative table longer than sum of arities");
@@ -245,12 +263,124 @@ void emit_op(Lowered& L, const TileMap& tm, const svg_gate& g, uint32_t kind_bas
   L.ops.push_back(op);
 }
 
+// (c0 I + c1 P)(d0 I + d1 P) with P^2 = I
+void pauli_mul(const svg_c128* x, const svg_c128* y, svg_c128* out) {
+  const double2 x0 = d2(x[0]), x1 = d2(x[1]), y0 = d2(y[0]), y1 = d2(y[1]);
+  const double2 a = cm(x0, y0), b = cm(x1, y1), c = cm(x0, y1), d = cm(x1, y0);
+  out[0] = svg_c128{a.x + b.x, a.y + b.y};
+  out[1] = svg_c128{c.x + d.x, c.y + d.y};
+  for (int i = 2; i < 16; ++i) out[i] = svg_c128{0.0, 0.0};
+}
+
+void mat_mul(const svg_c128* x, const svg_c128* y, int dim, svg_c128* out) {
+  svg_c128 r[16] = {};
+  for (int i = 0; i < dim; ++i)
+    for (int j = 0; j < dim; ++j) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = 0; k < dim; ++k) {
+        const double2 t = cm(d2(x[i * dim + k]), d2(y[k * dim + j]));
+        acc.x += t.x;
+        acc.y += t.y;
+      }
+      r[i * dim + j] = svg_c128{acc.x, acc.y};
+    }
+  for (int i = 0; i < 16; ++i) out[i] = r[i];
+}
+
+Gen make_gen(const svg_gate& g, const svg_deriv& dv) {
+  Gen gen;
+  const bool post = dv.basis == 1;
+  const svg_c128* given = dv.k;
+  svg_c128* other = post ? gen.pre : gen.post;
+  std::memcpy(post ? gen.post : gen.pre, given, sizeof(gen.pre));
+  // pre = post * U ; post = pre * R   (R = U^-1 on the control subspace)
+  const svg_c128* right = post ? g.fwd : g.rewind;
+  if (g.form == SVG_FORM_PAULI)
+    pauli_mul(given, right, other);
+  else
+    mat_mul(given, right, 1 << g.ntargets, other);
+  return gen;
+}
+
+bool is_dense(const svg_gate& g) { return g.form != SVG_FORM_PAULI || g.nderiv > 1; }
+
+// Segment-local bit of each tile position for a register segment.
+struct SegLocal {
+  uint8_t bit[32];
+  uint32_t conv(uint32_t tile_mask) const {
+    uint32_t r = 0;
+    for (uint32_t v = tile_mask; v; v &= v - 1) r |= 1u << bit[__builtin_ctz(v)];
+    return r;
+  }
+};
+
+SegDesc make_seg(int kind, uint32_t regmask, int k, SegLocal* sl) {
+  SegDesc sd;
+  std::memset(&sd, 0, sizeof(sd));
+  sd.kind = kind;
+  int r = 0, w = 0;
+  for (int pos = 0; pos < k; ++pos) {
+    if (pos < 5) {
+      sl->bit[pos] = static_cast<uint8_t>(pos);
+    } else if ((regmask >> pos) & 1) {
+      sd.regpos[r] = static_cast<uint8_t>(pos);
+      sl->bit[pos] = static_cast<uint8_t>(5 + r++);
+    } else {
+      sd.warppos[w] = static_cast<uint8_t>(pos);
+      sl->bit[pos] = static_cast<uint8_t>(5 + kRegBits + w++);
+    }
+  }
+  return sd;
+}
+
+// One register op for gate g: operator coefficients `c` (a, b of a I + b P),
+// optionally fused with the post-gate generator `kpost` into `slot`.
+void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate& g, uint32_t kind,
+              const svg_c128* c, const svg_c128* kpost, uint32_t slot, bool real_sums) {
+  RegOp op;
+  std::memset(&op, 0, sizeof(op));
+  op.kind = kind;
+  op.x = sl.conv(tm.local(g.x_mask));
+  op.z = sl.conv(tm.local(g.z_mask));
+  op.c = sl.conv(tm.local(g.ctrl_mask));
+  op.zo = g.z_mask & ~tm.qmask;
+  op.co = g.ctrl_mask & ~tm.qmask;
+  const double2 ph = ipow(g.n_y);
+  op.a = d2(c[0]);
+  op.b = cm(d2(c[1]), ph);
+  if (op.a.y == 0.0 && (op.b.x == 0.0 || op.b.y == 0.0)) {
+    op.flags |= RF_ROT;
+    if (op.b.x == 0.0 && op.b.y != 0.0) op.flags |= RF_BI;
+  }
+  if (kpost) {
+    op.flags |= RF_IP;
+    op.slot = slot;
+    op.ka = d2(kpost[0]);
+    op.kb = cm(d2(kpost[1]), ph);
+    const bool diag = op.ka.x != 0.0 || op.ka.y != 0.0;
+    if (diag) {
+      op.flags |= RF_IP_DIAG | RF_IP_RE | RF_IP_IM;
+    } else if (!real_sums) {
+      op.flags |= RF_IP_RE | RF_IP_IM;
+    } else {
+      if (op.kb.x != 0.0) op.flags |= RF_IP_RE;
+      if (op.kb.y != 0.0) op.flags |= RF_IP_IM;
+      if (!(op.flags & (RF_IP_RE | RF_IP_IM))) op.flags |= RF_IP_RE;
+    }
+  }
+  L.rops.push_back(op);
+}
+
 Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   Lowered L;
   const int n = p->num_qubits;
+  const bool real_sums = (p->flags & SVG_FLAG_REAL_SUMS) != 0;
   L.n = n;
   L.k = choose_tile_qubits(n, static_cast<int>(e->opt_tile), e->sms);
   L.b = (n <= L.k) ? n : std::min(5, L.k - 2);
+  const int wbits = L.k - 5 - kRegBits;
+  L.reg = e->opt_kernel != 1 && L.b >= 5 && wbits >= 0 && wbits <= 3;
+  if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need >= 9 tile qubits and <= 12");
   PlanParams pp;
   pp.n = n;
   pp.k = L.k;
@@ -264,15 +394,76 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   std::vector<int> first_deriv(p->num_gates + 1, 0);
   for (int i = 0; i < p->num_gates; ++i) first_deriv[i + 1] = first_deriv[i] + p->gates[i].nderiv;
+  std::vector<Gen> gens(p->num_derivs);
+  for (int d = 0; d < p->num_derivs; ++d) gens[d] = make_gen(p->gates[p->derivs[d].gate], p->derivs[d]);
+
+  // segments per pass (register path)
+  std::vector<std::vector<Segment>> psegs(gpasses.size());
+  if (L.reg) {
+    for (size_t pi = 0; pi < gpasses.size(); ++pi) {
+      const Pass& ps = gpasses[pi];
+      const TileMap tm = tile_map(ps.qmask);
+      std::vector<uint32_t> flips(ps.items.size());
+      std::vector<char> dense(ps.items.size());
+      for (size_t j = 0; j < ps.items.size(); ++j) {
+        const svg_gate& g = p->gates[ps.items[j]];
+        dense[j] = is_dense(g);
+        flips[j] = tm.local(shapes[ps.items[j]].flip);
+      }
+      psegs[pi] = plan_segments(flips, dense, L.k, kRegBits);
+    }
+  }
+  auto reg_launch = [&](const Pass& ps, int nb) {
+    Launch l;
+    l.d = make_desc(n, L.k, ps.qmask);
+    l.kind = L_REG;
+    l.nb = nb;
+    l.threads = 32 << wbits;
+    l.d.seg_begin = static_cast<int>(L.segs.size());
+    return l;
+  };
+  // default register layout for shared-memory segments: lowest non-lane positions
+  const uint32_t default_regs = ((1u << (5 + kRegBits)) - 1u) & ~31u;
 
   // forward passes
-  for (const Pass& ps : gpasses) {
+  for (size_t pi = 0; pi < gpasses.size(); ++pi) {
+    const Pass& ps = gpasses[pi];
     const TileMap tm = tile_map(ps.qmask);
-    Launch l{make_desc(n, L.k, ps.qmask), 0, 0};
-    l.d.op_begin = static_cast<int>(L.ops.size());
-    for (int gi : ps.items) emit_op(L, tm, p->gates[gi], OP_APPLY_PAULI, 0, p->gates[gi].fwd, 0);
-    l.d.op_end = static_cast<int>(L.ops.size());
-    L.fwd.push_back(l);
+    if (!L.reg) {
+      Launch l;
+      l.d = make_desc(n, L.k, ps.qmask);
+      l.kind = L_SMEM_FWD;
+      l.d.op_begin = static_cast<int>(L.ops.size());
+      for (int gi : ps.items) emit_op(L, tm, p->gates[gi], OP_APPLY_PAULI, 0, p->gates[gi].fwd, 0);
+      l.d.op_end = static_cast<int>(L.ops.size());
+      L.fwd.push_back(l);
+    } else {
+      Launch l = reg_launch(ps, 1);
+      uint32_t prev = ~0u;
+      for (const Segment& sg : psegs[pi]) {
+        SegLocal sl;
+        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, &sl);
+        sd.same_map = sg.reg && sg.regmask == prev;
+        prev = sg.reg ? sg.regmask : ~0u;
+        if (sg.reg) {
+          sd.op_begin = static_cast<int>(L.rops.size());
+          for (int it : sg.items) {
+            const svg_gate& g = p->gates[ps.items[it]];
+            emit_rop(L, tm, sl, g, ROP_FWD, g.fwd, nullptr, 0, real_sums);
+          }
+          sd.op_end = static_cast<int>(L.rops.size());
+        } else {
+          sd.op_begin = static_cast<int>(L.ops.size());
+          for (int it : sg.items) emit_op(L, tm, p->gates[ps.items[it]], OP_APPLY_PAULI, 0, p->gates[ps.items[it]].fwd, 0);
+          sd.op_end = static_cast<int>(L.ops.size());
+          l.tiles = true;
+        }
+        L.segs.push_back(sd);
+      }
+      l.d.seg_end = static_cast<int>(L.segs.size());
+      if (psegs[pi].size() > 1) l.tiles = true;
+      L.fwd.push_back(l);
+    }
     L.pass_bytes += 2 * S;
   }
 
@@ -291,9 +482,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   for (size_t j = 0; j < tpasses.size(); ++j) {
     const Pass& ps = tpasses[j];
     const TileMap tm = tile_map(ps.qmask);
-    Launch l{make_desc(n, L.k, ps.qmask), 0, 0};
+    Launch l;
+    l.d = make_desc(n, L.k, ps.qmask);
     l.d.op_begin = static_cast<int>(L.terms.size());
     l.d.untiled = ps.qmask == 0;
+    l.kind = l.d.untiled ? L_OBS_DIRECT : L_OBS;
     for (int ti : ps.items) {
       const svg_pauli_term& src = p->terms[ti];
       DevTerm dt;
@@ -317,54 +510,111 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   // reverse passes: forward passes backwards, gates backwards inside
   std::vector<std::pair<int, int>> deriv_slot(p->num_derivs, {-1, -1});  // (rev pass, slot)
+  auto smem_reverse_ops = [&](const TileMap& tm, int gi, uint32_t& slot) {
+    const svg_gate& g = p->gates[gi];
+    emit_op(L, tm, g, OP_APPLY_PAULI, 0, g.rewind, 0);
+    for (int j = 0; j < g.nderiv; ++j) {
+      const int d = first_deriv[gi] + j;
+      deriv_slot[d] = {static_cast<int>(L.rev.size()), static_cast<int>(slot)};
+      emit_op(L, tm, g, OP_IP_PAULI, 0, gens[d].pre, slot++);
+    }
+    if (gi > 0) emit_op(L, tm, g, OP_APPLY_PAULI, 1, g.adjoint, 0);
+  };
   if (with_reverse) {
     for (int pi = static_cast<int>(gpasses.size()) - 1; pi >= 0; --pi) {
       const Pass& ps = gpasses[pi];
       const TileMap tm = tile_map(ps.qmask);
-      Launch l{make_desc(n, L.k, ps.qmask), 0, 0};
-      l.d.op_begin = static_cast<int>(L.ops.size());
       uint32_t slot = 0;
-      for (auto it = ps.items.rbegin(); it != ps.items.rend(); ++it) {
-        const int gi = *it;
-        const svg_gate& g = p->gates[gi];
-        emit_op(L, tm, g, OP_APPLY_PAULI, 0, g.rewind, 0);
-        for (int j = 0; j < g.nderiv; ++j) {
-          const int d = first_deriv[gi] + j;
-          deriv_slot[d] = {static_cast<int>(L.rev.size()), static_cast<int>(slot)};
-          emit_op(L, tm, g, OP_IP_PAULI, 0, p->derivs[d].k, slot++);
+      if (!L.reg) {
+        Launch l;
+        l.d = make_desc(n, L.k, ps.qmask);
+        l.kind = L_SMEM_REV;
+        l.d.op_begin = static_cast<int>(L.ops.size());
+        for (auto it = ps.items.rbegin(); it != ps.items.rend(); ++it) smem_reverse_ops(tm, *it, slot);
+        l.d.op_end = static_cast<int>(L.ops.size());
+        l.d.nslots = static_cast<int>(slot);
+        L.rev.push_back(l);
+      } else {
+        Launch l = reg_launch(ps, 2);
+        const std::vector<Segment>& sgs = psegs[pi];
+        uint32_t prev = ~0u;
+        for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
+          const Segment& sg = *st;
+          SegLocal sl;
+          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, &sl);
+          sd.same_map = sg.reg && sg.regmask == prev;
+          prev = sg.reg ? sg.regmask : ~0u;
+          if (sg.reg) {
+            sd.op_begin = static_cast<int>(L.rops.size());
+            for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it) {
+              const int gi = ps.items[*it];
+              const svg_gate& g = p->gates[gi];
+              const svg_c128* kpost = nullptr;
+              if (g.nderiv == 1) {
+                const int d = first_deriv[gi];
+                deriv_slot[d] = {static_cast<int>(L.rev.size()), static_cast<int>(slot)};
+                kpost = gens[d].post;
+              }
+              emit_rop(L, tm, sl, g, ROP_REV, g.rewind, kpost, kpost ? slot++ : 0, real_sums);
+              if (gi > 0) emit_rop(L, tm, sl, g, ROP_LAM, g.adjoint, nullptr, 0, real_sums);
+            }
+            sd.op_end = static_cast<int>(L.rops.size());
+          } else {
+            sd.op_begin = static_cast<int>(L.ops.size());
+            for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it) smem_reverse_ops(tm, ps.items[*it], slot);
+            sd.op_end = static_cast<int>(L.ops.size());
+            l.tiles = true;
+          }
+          L.segs.push_back(sd);
         }
-        if (gi > 0) emit_op(L, tm, g, OP_APPLY_PAULI, 1, g.adjoint, 0);
+        l.d.seg_end = static_cast<int>(L.segs.size());
+        if (sgs.size() > 1) l.tiles = true;
+        l.d.nslots = static_cast<int>(slot);
+        L.rev.push_back(l);
       }
-      l.d.op_end = static_cast<int>(L.ops.size());
-      l.d.nslots = static_cast<int>(slot);
-      L.rev.push_back(l);
       L.pass_bytes += 4 * S;
     }
   }
 
   // grids, shared memory, partial offsets
   const int64_t ntiles = int64_t(1) << (n - L.k);
-  auto grid_for = [&](int which, size_t smem) {
-    const int64_t slots = int64_t(e->sms) * occupancy(which, smem);
+  auto clamp_grid = [&](int per_sm) {
+    const int64_t slots = int64_t(e->sms) * per_sm;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, slots)));
   };
-  for (Launch& l : L.fwd) {
-    l.smem = fwd_smem(L.k, l.d.b);
-    l.grid = grid_for(0, l.smem);
-  }
+  auto size_launch = [&](Launch& l) {
+    switch (l.kind) {
+      case L_SMEM_FWD:
+        l.smem = fwd_smem(L.k, l.d.b);
+        l.grid = clamp_grid(occupancy(0, l.smem));
+        break;
+      case L_SMEM_REV:
+        l.smem = rev_smem(L.k, l.d.b, l.d.nslots);
+        l.grid = clamp_grid(occupancy(2, l.smem));
+        break;
+      case L_REG:
+        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.tiles);
+        l.grid = clamp_grid(reg_occupancy(l.nb, l.threads, l.smem));
+        break;
+      case L_OBS:
+        l.smem = obs_smem(L.k, l.d.b);
+        l.grid = clamp_grid(occupancy(1, l.smem));
+        break;
+      default:
+        l.smem = 0;
+        l.grid = std::max(1, static_cast<int>(std::min<int64_t>(int64_t(e->sms) * 8, int64_t(1) << std::max(0, n - 8))));
+    }
+    if (l.smem > e->max_smem) throw InvalidArg("pass needs more shared memory than the device offers");
+  };
+  for (Launch& l : L.fwd) size_launch(l);
   for (Launch& l : L.obs) {
-    l.smem = l.d.untiled ? 0 : obs_smem(L.k, l.d.b);
-    l.grid = l.d.untiled ? std::max(1, std::min<int>(e->sms * 8, static_cast<int>(std::min<int64_t>(
-                               int64_t(1) << std::max(0, n - 8), 1 << 30))))
-                         : grid_for(1, l.smem);
+    size_launch(l);
     l.d.part_off = part;
     part += l.grid;
   }
   const int64_t energy_count = part - energy_off;
   for (Launch& l : L.rev) {
-    l.smem = rev_smem(L.k, l.d.b, l.d.nslots);
-    if (l.smem > e->max_smem) throw InvalidArg("pass needs more shared memory than the device offers");
-    l.grid = grid_for(2, l.smem);
+    size_launch(l);
     l.d.part_off = part;
     part += int64_t(l.d.nslots) * l.grid;
   }
@@ -383,7 +633,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 }
 
 struct Blob {
-  size_t ops, coef, terms, sums, total;
+  size_t ops, coef, terms, sums, rops, segs, total;
 };
 
 Blob layout(const Lowered& L) {
@@ -397,6 +647,10 @@ Blob layout(const Lowered& L) {
   o = align_up(o + L.terms.size() * sizeof(DevTerm), 256);
   b.sums = o;
   o = align_up(o + L.sums.size() * sizeof(SumSpec), 256);
+  b.rops = o;
+  o = align_up(o + L.rops.size() * sizeof(RegOp), 256);
+  b.segs = o;
+  o = align_up(o + L.segs.size() * sizeof(SegDesc), 256);
   b.total = std::max<size_t>(o, 256);
   return b;
 }
@@ -435,6 +689,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     std::memcpy(hb + bl.coef, L.coef.data(), L.coef.size() * sizeof(double2));
     std::memcpy(hb + bl.terms, L.terms.data(), L.terms.size() * sizeof(DevTerm));
     std::memcpy(hb + bl.sums, L.sums.data(), L.sums.size() * sizeof(SumSpec));
+    std::memcpy(hb + bl.rops, L.rops.data(), L.rops.size() * sizeof(RegOp));
+    std::memcpy(hb + bl.segs, L.segs.data(), L.segs.size() * sizeof(SegDesc));
 
     double2* psi = static_cast<double2*>(e->psi.ptr);
     double2* lam = static_cast<double2*>(e->lam.ptr);
@@ -443,6 +699,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     const double2* dcoef = reinterpret_cast<const double2*>(db + bl.coef);
     const DevTerm* dterms = reinterpret_cast<const DevTerm*>(db + bl.terms);
     const SumSpec* dsums = reinterpret_cast<const SumSpec*>(db + bl.sums);
+    const RegOp* drops = reinterpret_cast<const RegOp*>(db + bl.rops);
+    const SegDesc* dsegs = reinterpret_cast<const SegDesc*>(db + bl.segs);
     double2* dres = static_cast<double2*>(e->results.ptr);
 
     int64_t launches = 0, h2d = bl.total, d2h = L.sums.size() * sizeof(double2);
@@ -457,7 +715,12 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       launches += 1;
     }
     CK(cudaEventRecord(e->ev[1], s));
-    for (const Launch& l : L.fwd) launch_fwd(l.d, l.grid, l.smem, s, psi, dops, dcoef);
+    for (const Launch& l : L.fwd) {
+      if (l.kind == L_REG)
+        launch_pass_reg(1, l.d, l.grid, l.threads, l.smem, s, psi, nullptr, dsegs, drops, dops, dcoef, part);
+      else
+        launch_fwd(l.d, l.grid, l.smem, s, psi, dops, dcoef);
+    }
     CK(cudaEventRecord(e->ev[2], s));
     for (const Launch& l : L.obs) {
       if (l.d.untiled)
@@ -466,7 +729,12 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         launch_obs(l.d, l.grid, l.smem, s, psi, lam, dterms, part);
     }
     CK(cudaEventRecord(e->ev[3], s));
-    for (const Launch& l : L.rev) launch_rev(l.d, l.grid, l.smem, s, psi, lam, dops, dcoef, part);
+    for (const Launch& l : L.rev) {
+      if (l.kind == L_REG)
+        launch_pass_reg(2, l.d, l.grid, l.threads, l.smem, s, psi, lam, dsegs, drops, dops, dcoef, part);
+      else
+        launch_rev(l.d, l.grid, l.smem, s, psi, lam, dops, dcoef, part);
+    }
     CK(cudaEventRecord(e->ev[4], s));
     launch_finalize(part, dsums, static_cast<int>(L.sums.size()), dres, s);
     CK(cudaGetLastError());
@@ -561,6 +829,7 @@ int svg_engine_create(int device, svg_engine** out) {
     e->sms = prop.multiProcessorCount;
     e->max_smem = prop.sharedMemPerBlockOptin;
     CK(prepare_kernels(e->max_smem));
+    CK(prepare_reg_kernels(e->max_smem));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
     e->stream = e->own_stream;
     for (auto& ev : e->ev) CK(cudaEventCreate(&ev));
@@ -607,6 +876,9 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     e->opt_tile = value;
   } else if (k == "profile") {
     e->opt_profile = value;
+  } else if (k == "kernel") {
+    if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
+    e->opt_kernel = value;
   } else if (k == "max_gates_per_pass") {
     if (value < 0) return fail(SVG_EINVAL, "max_gates_per_pass must be >= 0");
     e->opt_max_items = value;

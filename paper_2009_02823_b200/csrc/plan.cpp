@@ -94,6 +94,45 @@ std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, cons
   return passes;
 }
 
+std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<char>& dense, int k,
+                                   int regbits) {
+  const uint32_t lanes = 31u;
+  const uint32_t nonlane = ((k >= 32) ? ~0u : ((1u << k) - 1)) & ~lanes;
+  std::vector<Segment> segs;
+  Segment cur;
+  auto flush = [&]() {
+    if (!cur.items.empty()) segs.push_back(cur);
+    cur = Segment();
+  };
+  const int m = static_cast<int>(flip_pos.size());
+  for (int i = 0; i < m; ++i) {
+    if (dense[i]) {
+      if (cur.reg) flush();
+      cur.reg = false;
+      cur.items.push_back(i);
+      continue;
+    }
+    if (!cur.reg) flush();
+    const uint32_t f = flip_pos[i] & nonlane;
+    if (popc(cur.regmask | f) > regbits) flush();
+    cur.regmask |= f;
+    cur.items.push_back(i);
+  }
+  flush();
+  // Fill each register set to exactly `regbits` positions, preferring the
+  // positions the following segments flip (fewer distinct layouts overall).
+  for (size_t s = 0; s < segs.size(); ++s) {
+    if (!segs[s].reg) continue;
+    uint32_t& rm = segs[s].regmask;
+    for (size_t t = s + 1; t < segs.size() && popc(rm) < regbits; ++t) {
+      if (!segs[t].reg) continue;
+      for (uint32_t v = segs[t].regmask & ~rm; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+    }
+    for (uint32_t v = nonlane & ~rm; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+  }
+  return segs;
+}
+
 int choose_tile_qubits(int n, int requested, int sms) {
   if (requested > 0) return std::min(requested, n);
   if (n <= 10) return n;  // whole state in one tile: one CTA, no HBM round trips between passes

@@ -54,6 +54,18 @@ std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const P
 std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp,
                                    std::vector<int>* direct);
 
+// Register segments of one pass (register-tile kernels).  Tile positions
+// 0..4 are lanes; a segment picks `regbits` of the other positions as
+// register bits (the rest are warp bits, which its gates may not flip).
+// Dense-matrix gates form shared-memory segments of their own.
+struct Segment {
+  bool reg = true;
+  std::vector<int> items;   // indices into the pass's item list
+  uint32_t regmask = 0;     // tile positions held in registers (reg segments)
+};
+std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<char>& dense, int k,
+                                   int regbits);
+
 // Tile size choice for n qubits on `sms` SMs (auto when requested == 0).
 int choose_tile_qubits(int n, int requested, int sms);
 

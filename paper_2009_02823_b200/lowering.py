@@ -7,9 +7,10 @@ svgrad/circuit.py:228-334) restated as flat, device-ready tables:
 * Pauli-form gates (every ``PauliRotation``, and ``FixedUnitary`` X/Y/Z incl.
   CX/CY/CZ) become ``op = a*I + b*P`` with the gate's Pauli product P:
   ``U = cos(alpha*theta) I + i sin(alpha*theta) P`` (svgrad/gates.py:42-50),
-  ``U^-1 = U^dag = conj(a) I + conj(b) P``, and the derivative generator
-  relative to the pre-gate state, ``K = alpha*i * P U = alpha*i*(b I + a P)``
-  (the reference applies P then U and defers alpha*i, svgrad/circuit.py:316-321).
+  ``U^-1 = U^dag = conj(a) I + conj(b) P``, and the derivative generator in
+  the post-gate basis (svg_deriv.basis = 1), ``K' = alpha*i * P``: the
+  reference's probe is ``alpha*i * U P phi_i = alpha*i * P phi_{i+1}``
+  (it applies P then U and defers alpha*i, svgrad/circuit.py:316-321).
 * Dense-matrix gates (``Phase``, other ``FixedUnitary``, ``CustomParametric``,
   ``NonUnitary``) ship U, the rewind (adjoint, or the true inverse for
   NonUnitary -> ``NonInvertibleGateError`` text identical to
@@ -42,7 +43,7 @@ GATE_DTYPE = np.dtype(
     align=True,
 )
 DERIV_DTYPE = np.dtype(
-    [("gate", "<i4"), ("param_ref", "<i4"), ("form", "<i4"), ("reserved", "<i4"), ("k", "<c16", (16,))],
+    [("gate", "<i4"), ("param_ref", "<i4"), ("form", "<i4"), ("basis", "<i4"), ("k", "<c16", (16,))],
     align=True,
 )
 TERM_DTYPE = np.dtype(
@@ -50,6 +51,7 @@ TERM_DTYPE = np.dtype(
     align=True,
 )
 _PAULI_FIXED = {"X": SIGMA["X"], "Y": SIGMA["Y"], "Z": SIGMA["Z"]}
+FLAG_REAL_SUMS = 1  # SVG_FLAG_REAL_SUMS: only 2*Re(sums) is consumed (Hermitian observables)
 
 
 @dataclass
@@ -157,9 +159,9 @@ def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
         gates["rewind"][st.rot_gates, 1] = np.conj(b)
         gates["adjoint"][st.rot_gates, 0] = np.conj(a)
         gates["adjoint"][st.rot_gates, 1] = np.conj(b)
-        coef = (st.rot_alpha * 1j) * scale
-        derivs["k"][st.rot_derivs, 0] = coef * b
-        derivs["k"][st.rot_derivs, 1] = coef * a
+        # post-gate generator (basis 1): dU phi_i = alpha*i P U phi_i = alpha*i P phi_{i+1}
+        derivs["k"][st.rot_derivs, 1] = (st.rot_alpha * 1j) * scale
+        derivs["basis"][st.rot_derivs] = 1
     if st.fixed_pauli.size:
         for field in ("fwd", "rewind", "adjoint"):
             gates[field][st.fixed_pauli, 1] = 1.0
@@ -201,7 +203,7 @@ def lower_terms(obs) -> np.ndarray:
 class Problem:
     """Owns the numpy tables and the svg_problem that points into them."""
 
-    def __init__(self, circuit, params, obs, input_state, with_derivs: bool = True):
+    def __init__(self, circuit, params, obs, input_state, real_sums: bool = False):
         self.gates, self.derivs = bind(circuit, params)
         self.terms = lower_terms(obs)
         self.num_derivs = len(self.derivs)
@@ -217,6 +219,7 @@ class Problem:
         p.num_gates = len(self.gates)
         p.num_derivs = self.num_derivs
         p.num_terms = len(self.terms)
+        p.flags = FLAG_REAL_SUMS if real_sums else 0
         p.gates = self.gates.ctypes.data_as(C.POINTER(N.svg_gate))
         p.derivs = self.derivs.ctypes.data_as(C.POINTER(N.svg_deriv))
         p.terms = self.terms.ctypes.data_as(C.POINTER(N.svg_pauli_term))

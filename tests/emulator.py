@@ -87,10 +87,15 @@ def emulate(circuit, params, obs, input_state, tile_qubits=0, sms=0):
     for p in range(len(start) - 2, -1, -1):
         for gi in order[start[p]: start[p + 1]][::-1]:
             g = gates[gi]
+            for j in range(int(g["nderiv"])):  # generators in the post-gate basis see phi_{i+1}
+                d = first[gi] + j
+                if derivs[d]["basis"] == 1:
+                    contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
             psi = _apply(psi, g, "rewind")
             for j in range(int(g["nderiv"])):
                 d = first[gi] + j
-                contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
+                if derivs[d]["basis"] == 0:
+                    contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
             if gi > 0:
                 lam = _apply(lam, g, "adjoint")
     sums = np.zeros(circuit.num_params, dtype=complex)

@@ -64,6 +64,54 @@ def test_tile_size_invariance(tile):
     assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
 
 
+def _with_options(opts, fn):
+    eng = sv._native.engine()
+    for k, v in opts.items():
+        eng.set_option(k, v)
+    try:
+        return fn()
+    finally:
+        for k in opts:
+            eng.set_option(k, 0)
+
+
+@pytest.mark.parametrize("name", ["cfg2_n12", "cfg3_n14", "cfg4_n16", "cfg5_n15", "cfg1"])
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_both_kernel_families_match_golden(name, kernel):
+    """Shared-memory tiles (1) and register tiles (2) against the reference's outputs."""
+    rec = GOLD[name]
+    circ, theta, obs, inp, _ = materialize(SMALL[name])
+    rep = _with_options({"kernel": kernel}, lambda: sv.reverse_mode_gradient(circ, theta, obs, inp))
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("n", [9, 10, 12])
+@pytest.mark.parametrize("method", ["reverse", "non_hermitian"])
+def test_every_gate_kind_in_register_tiles(n, method):
+    """Dense-matrix gates (shared-memory segments), controls, 2-qubit Paulis, repeated
+    parameters and complex generators, at sizes that use the register-tile kernels."""
+    from cases import all_kinds_circuit, mixed_observable, random_amplitudes
+    from oracle import oracle
+
+    circ = all_kinds_circuit(sv, n)
+    theta = np.random.default_rng([5, n]).uniform(-np.pi, 2 * np.pi, circ.num_params)
+    complex_obs = method == "non_hermitian"
+    obs = mixed_observable(sv, n, 21, count=12, letters="XYZ+-" if complex_obs else "XYZH", complex_coeffs=complex_obs)
+    inp = sv.StateVector(n, random_amplitudes(n, 9))
+    for tile in (0, 9, 10):
+        if tile > n:
+            continue
+        if complex_obs:
+            rep = _with_options({"tile_qubits": tile}, lambda: sv.non_hermitian_gradient(circ, theta, obs, inp))
+            vals, energy, _ = oracle.non_hermitian_values(circ, theta, obs, inp.amplitudes)
+        else:
+            rep = _with_options({"tile_qubits": tile}, lambda: sv.reverse_mode_gradient(circ, theta, obs, inp))
+            vals, energy, _ = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+        assert max_err(rep.values, vals) <= GRAD_TOL, tile
+        assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
 def test_pass_cap_invariance():
     circ, theta, obs, inp, _ = materialize(SMALL["cfg3_n14"])
     eng = sv._native.engine()

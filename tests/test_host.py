@@ -98,8 +98,10 @@ def test_pauli_lowering_of_rotations():
         R = gates[i]["rewind"][0] * np.eye(P.shape[0]) + gates[i]["rewind"][1] * P
         assert np.allclose(R @ U, np.eye(P.shape[0]), atol=1e-15)
         K = derivs[i]["k"][0] * np.eye(P.shape[0]) + derivs[i]["k"][1] * P
-        # reference derivative action: sigma per axis, then the bound rotation, scalar alpha*i
-        assert np.allclose(K, g.kind.alpha * 1j * (U @ P), atol=1e-15)
+        # reference derivative action: sigma per axis, then the bound rotation, scalar alpha*i,
+        # acting on phi_i; the table holds it in the post-gate basis: K' = K_pre U^-1
+        assert derivs[i]["basis"] == 1
+        assert np.allclose(K @ U, g.kind.alpha * 1j * (U @ P), atol=1e-15)
 
 
 def test_non_pauli_observable_letters_expand_exactly():
