@@ -308,12 +308,18 @@ size_t reg_smem(int k, int nb, int nwarps, int nslots, bool tiles) {
   return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0));
 }
 
-cudaError_t prepare_reg_kernels(size_t max_smem) {
-  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k_pass_reg<kRegBits, 1>),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(max_smem));
+static cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaFuncGetAttributes(&attr, fn);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(reinterpret_cast<const void*>(k_pass_reg<kRegBits, 2>),
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(max_smem));
+  const size_t room = max_smem > attr.sharedSizeBytes ? max_smem - attr.sharedSizeBytes : 0;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(room));
+}
+
+cudaError_t prepare_reg_kernels(size_t max_smem) {
+  cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(k_pass_reg<kRegBits, 1>), max_smem);
+  if (e != cudaSuccess) return e;
+  return allow_dynamic_smem(reinterpret_cast<const void*>(k_pass_reg<kRegBits, 2>), max_smem);
 }
 
 int reg_occupancy(int nb, int threads, size_t smem) {
