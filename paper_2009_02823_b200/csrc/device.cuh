@@ -70,28 +70,43 @@ struct PassDesc {
 // bits (warp shuffles) and register bits (register permutations) but never
 // warp bits; between segments the tile is transposed through shared memory.
 
+// Every register op is a Pauli-form operator with real a and real-or-imaginary
+// b' (all rotations, X/Y/Z, CX..., daggers of those):
+//     new[t] = a v[t] + bb * (-1)^s(t) * (i^BI) v[t ^ x]
+// where s(t) = parity((t ^ x) & z) ^ parity(base & zo).  The sign of the
+// register part of t is precomputed per register slot (smask), so the device
+// only adds the lane/warp part.  Controls likewise (cmask + clw).
 enum RegOpKind : uint32_t {
-  ROP_FWD = 0,  // psi <- a psi + b' Psign psi                                   (forward)
-  ROP_REV = 1,  // [slot += <lam| K' |phi>]; phi <- a phi + b' Psign phi          (reverse, rewind)
-  ROP_LAM = 2,  // lam <- a lam + b' Psign lam                                    (reverse, adjoint)
+  ROP_FWD = 0,  // psi <- op psi                                     (forward)
+  ROP_REV = 1,  // [slot += <lam| K' |phi>]; phi <- op phi            (reverse: IP + rewind)
+  ROP_LAM = 2,  // lam <- op lam                                      (reverse: adjoint)
 };
 enum RegOpFlags : uint32_t {
-  RF_IP = 1u,       // ROP_REV accumulates the generator term before rewinding
-  RF_IP_RE = 2u,    // accumulate Re(z)
-  RF_IP_IM = 4u,    // accumulate Im(z)
-  RF_IP_DIAG = 8u,  // K' has an identity part ka: also accumulate z2 = sum conj(lam) phi
-  RF_ROT = 16u,     // a is real and b' is real (or imaginary with RF_BI): 4-flop update
-  RF_BI = 32u,      // b' is imaginary: multiply the partner by i and use b'.y
+  RF_IP1 = 1u,    // ROP_REV: accumulate one real component q = Re(conj(lam) sel(P phi))
+  RF_IP3 = 2u,    // ROP_REV: accumulate the full complex z and z2 = <lam|phi> (complex / diag K')
+  RF_BI = 4u,     // partner multiplied by i in the update (b' imaginary)
+  RF_KBI = 8u,    // RF_IP1: select -i * partner (Im part) for the inner product
+  RF_CTRL = 16u,  // op has controls inside the tile
+};
+enum RegOpShape : uint32_t {
+  RS_DIAG = 0,   // no flip
+  RS_LANE = 1,   // flip on lane bits only (warp shuffles)
+  RS_REG = 2,    // flip on exactly one register bit (xr) -> register pairs
 };
 
 struct RegOp {
-  uint32_t kind, flags;
-  uint32_t x, z, c;  // segment-local flip / sign / control masks
+  uint32_t kind, flags, shape;
+  uint32_t xl;        // lane flip mask
+  uint32_t xr;        // register flip mask (one bit) for RS_REG
+  uint32_t zlw;       // sign mask on lane | warp bits (segment-local)
+  uint32_t clw;       // control mask on lane | warp bits (segment-local)
+  uint32_t smask;     // bit j: parity((j ^ xr) & z_reg)     (register part of the partner sign)
+  uint32_t cmask;     // bit j: (j & c_reg) == c_reg        (register part of the control test)
   uint32_t slot;
-  uint64_t pad;
-  uint64_t zo, co;   // non-tile (global) sign / control masks
-  double2 a, b;      // operator a I + b' Psign  (b' includes i^{n_y})
-  double2 ka, kb;    // generator ka I + kb' Psign, relative to the post-gate state
+  uint64_t zo, co;    // non-tile (global) sign / control masks
+  double a, bb;       // operator coefficients (see above)
+  double kr;          // RF_IP1: contribution = kr * q (real part only)
+  double2 ka, kb;     // RF_IP3: contribution = kb' z + ka z2
 };
 static_assert(sizeof(RegOp) == 112, "RegOp layout");
 

@@ -302,8 +302,6 @@ Gen make_gen(const svg_gate& g, const svg_deriv& dv) {
   return gen;
 }
 
-bool is_dense(const svg_gate& g) { return g.form != SVG_FORM_PAULI || g.nderiv > 1; }
-
 // Segment-local bit of each tile position for a register segment.
 struct SegLocal {
   uint8_t bit[32];
@@ -340,35 +338,63 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
   RegOp op;
   std::memset(&op, 0, sizeof(op));
   op.kind = kind;
-  op.x = sl.conv(tm.local(g.x_mask));
-  op.z = sl.conv(tm.local(g.z_mask));
-  op.c = sl.conv(tm.local(g.ctrl_mask));
+  const uint32_t regbits = ((1u << kRegBits) - 1u) << 5;
+  const uint32_t xloc = sl.conv(tm.local(g.x_mask));
+  const uint32_t zloc = sl.conv(tm.local(g.z_mask));
+  const uint32_t cloc = sl.conv(tm.local(g.ctrl_mask));
+  op.xl = xloc & 31u;
+  op.xr = (xloc & regbits) >> 5;
+  op.shape = xloc == 0 ? RS_DIAG : (op.xr == 0 ? RS_LANE : RS_REG);
+  op.zlw = zloc & ~regbits;
+  op.clw = cloc & ~regbits;
+  const uint32_t zr = (zloc & regbits) >> 5, cr = (cloc & regbits) >> 5;
+  for (uint32_t j = 0; j < (1u << kRegBits); ++j) {
+    op.smask |= static_cast<uint32_t>(__builtin_popcount((j ^ op.xr) & zr) & 1) << j;
+    op.cmask |= static_cast<uint32_t>((j & cr) == cr) << j;
+  }
+  if (cloc) op.flags |= RF_CTRL;
   op.zo = g.z_mask & ~tm.qmask;
   op.co = g.ctrl_mask & ~tm.qmask;
   const double2 ph = ipow(g.n_y);
-  op.a = d2(c[0]);
-  op.b = cm(d2(c[1]), ph);
-  if (op.a.y == 0.0 && (op.b.x == 0.0 || op.b.y == 0.0)) {
-    op.flags |= RF_ROT;
-    if (op.b.x == 0.0 && op.b.y != 0.0) op.flags |= RF_BI;
+  const double2 b = cm(d2(c[1]), ph);
+  op.a = c[0].re;
+  if (b.x == 0.0 && b.y != 0.0) {
+    op.flags |= RF_BI;
+    op.bb = b.y;
+  } else {
+    op.bb = b.x;
   }
   if (kpost) {
-    op.flags |= RF_IP;
     op.slot = slot;
     op.ka = d2(kpost[0]);
     op.kb = cm(d2(kpost[1]), ph);
     const bool diag = op.ka.x != 0.0 || op.ka.y != 0.0;
-    if (diag) {
-      op.flags |= RF_IP_DIAG | RF_IP_RE | RF_IP_IM;
-    } else if (!real_sums) {
-      op.flags |= RF_IP_RE | RF_IP_IM;
+    if (real_sums && !diag && op.kb.y == 0.0) {
+      op.flags |= RF_IP1;
+      op.kr = op.kb.x;  // Re(kb' z) = kb'.x Re(z)
+    } else if (real_sums && !diag && op.kb.x == 0.0) {
+      op.flags |= RF_IP1 | RF_KBI;
+      op.kr = -op.kb.y;  // Re(i kappa z) = -kappa Im(z)
     } else {
-      if (op.kb.x != 0.0) op.flags |= RF_IP_RE;
-      if (op.kb.y != 0.0) op.flags |= RF_IP_IM;
-      if (!(op.flags & (RF_IP_RE | RF_IP_IM))) op.flags |= RF_IP_RE;
+      op.flags |= RF_IP3;
     }
   }
   L.rops.push_back(op);
+}
+
+// Whether a gate runs as a register op: Pauli form with a real a and a real or
+// imaginary b' in all three operators, at most one parameter, and a flip that
+// touches lanes only or exactly one non-lane tile position.
+bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
+  if (g.form != SVG_FORM_PAULI || g.nderiv > 1) return false;
+  const double2 ph = ipow(g.n_y);
+  for (const svg_c128* c : {g.fwd, g.rewind, g.adjoint}) {
+    const double2 b = cm(d2(c[1]), ph);
+    if (c[0].im != 0.0 || (b.x != 0.0 && b.y != 0.0)) return false;
+  }
+  const uint32_t hi = flip_tile & ~31u;
+  if (hi == 0) return true;
+  return __builtin_popcount(hi) == 1 && (flip_tile & 31u) == 0;
 }
 
 Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
@@ -379,8 +405,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   L.k = choose_tile_qubits(n, static_cast<int>(e->opt_tile), e->sms);
   L.b = (n <= L.k) ? n : std::min(5, L.k - 2);
   const int wbits = L.k - 5 - kRegBits;
-  L.reg = e->opt_kernel != 1 && L.b >= 5 && wbits >= 0 && wbits <= 3;
-  if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need >= 9 tile qubits and <= 12");
+  L.reg = e->opt_kernel != 1 && L.b >= 5 && wbits >= 0 && (32 << wbits) <= reg_max_threads();
+  if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 9..11 tile qubits");
   PlanParams pp;
   pp.n = n;
   pp.k = L.k;
@@ -407,8 +433,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       std::vector<char> dense(ps.items.size());
       for (size_t j = 0; j < ps.items.size(); ++j) {
         const svg_gate& g = p->gates[ps.items[j]];
-        dense[j] = is_dense(g);
         flips[j] = tm.local(shapes[ps.items[j]].flip);
+        dense[j] = !reg_capable(g, flips[j]);
       }
       psegs[pi] = plan_segments(flips, dense, L.k, kRegBits);
     }

@@ -1,17 +1,19 @@
-// Register-tile pass kernel (v2) for sm_100a: the hot K1/K3 path.
+// Register-tile pass kernel for sm_100a: the hot K1/K3 path.
 //
 // One CTA processes 2^k-amplitude tiles (k = 5 lane + R register + w warp
 // bits, see device.cuh).  Per tile:
 //   global -> registers (512-byte coalesced rows: lanes are qubits 0..4)
 //   for each segment: run its Pauli-form gates entirely in registers --
-//       register-bit flips are register permutations, lane-bit flips are
-//       warp shuffles, diagonal factors and controls are index predicates;
-//       the reverse step fuses  slot += <lam|K'|phi>,  phi <- R phi  on the
-//       same partner values, then  lam <- U^dag lam  (svgrad/gradients.py:158-168,
-//       generator form of svgrad/circuit.py:316-334; mu never exists);
+//       register-bit flips are register pairs (one code path per flipped
+//       register bit), lane-bit flips are warp shuffles, Z factors and
+//       controls are sign / predicate bits precomputed on the host per
+//       register slot; the reverse step fuses  slot += <lam|K'|phi>  and
+//       phi <- R phi  on the same partner values, then  lam <- U^dag lam
+//       (svgrad/gradients.py:158-168; generator form of svgrad/circuit.py:316-334;
+//       the probe mu never exists);
 //   between segments: transpose through shared memory (one barrier);
-//   dense-matrix gates (rare: Phase, H, callables) run on the shared-memory
-//   tile with the generic tile ops;
+//   dense-matrix gates (Phase, H, callables, 2-bit register flips) run on
+//   the shared-memory tile with the generic tile ops;
 //   registers -> global.
 // A pass with one register segment touches shared memory only for the
 // per-warp inner-product accumulators.
@@ -26,9 +28,16 @@ namespace svgb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kRegThreads = 128;  // launch bound: k = 11 tiles (4 warps)
 
 __device__ __forceinline__ double2 shfl2(double2 v, uint32_t m) {
   return make_double2(__shfl_xor_sync(kFull, v.x, m), __shfl_xor_sync(kFull, v.y, m));
+}
+// flip the sign of both components when bit `s` (0/1) is set (sign-bit xor, no FP op)
+__device__ __forceinline__ double2 sflip(double2 v, uint32_t s) {
+  const long long m = static_cast<long long>(s) << 63;
+  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
+                      __longlong_as_double(__double_as_longlong(v.y) ^ m));
 }
 
 template <int R>
@@ -95,97 +104,115 @@ __device__ __forceinline__ void from_smem(double2 (&v)[1 << R], const double2* s
   for (int j = 0; j < (1 << R); ++j) v[j] = s[row | soff(m, j)];
 }
 
-// new = a v + (+-b') p ; ROT: a real, b' real (BI: imaginary -> use i*p and b'.y)
-template <bool ROT>
-__device__ __forceinline__ double2 combine(double2 a, double2 b, bool bi, double2 v, double2 p, int s) {
-  if (ROT) {
-    double bb = bi ? b.y : b.x;
-    if (s) bb = -bb;
-    const double px = bi ? -p.y : p.x, py = bi ? p.x : p.y;
-    return make_double2(fma(a.x, v.x, bb * px), fma(a.x, v.y, bb * py));
-  }
-  return cfma(cneg_if(b, s), p, cmul(a, v));
+// Per-op, per-thread constants.
+struct OpCtx {
+  double a, bb;
+  uint32_t slw;   // lane/warp/base part of the partner sign (0/1)
+  uint32_t smask, cmask;
+  bool clw_ok;    // lane/warp part of the control test
+  bool bi, kbi;
+};
+
+// One amplitude: v <- a v + bb * (i^BI) * p_signed   (p_signed already carries the sign)
+__device__ __forceinline__ double2 upd(const OpCtx& c, double2 v, double2 ps) {
+  const double px = c.bi ? -ps.y : ps.x, py = c.bi ? ps.x : ps.y;
+  return make_double2(fma(c.bb, px, c.a * v.x), fma(c.bb, py, c.a * v.y));
 }
 
-// IPK: 0 none, 1 Re(z) only, 2 Im(z) only, 3 full complex z and z2
+// Inner-product terms for one amplitude with signed partner ps.
 template <int IPK>
-__device__ __forceinline__ void accumulate(double2& z, double2& z2, double2 lam, double2 p, double2 v, int s) {
-  if (IPK == 0) return;
-  const double px = s ? -p.x : p.x, py = s ? -p.y : p.y;
-  if (IPK == 1 || IPK == 3) z.x = fma(lam.x, px, fma(lam.y, py, z.x));
-  if (IPK == 2 || IPK == 3) z.y = fma(lam.x, py, fma(-lam.y, px, z.y));
-  if (IPK == 3) z2 = cjfma(lam, v, z2);
+__device__ __forceinline__ void ip_term(const OpCtx& c, double lamx, double lamy, double2 ps, double2 v, double& q,
+                                        double2& z, double2& z2) {
+  if (IPK == 1) {  // q += Re(conj(lam) * sel(ps)), sel = identity or -i
+    const double sx = c.kbi ? ps.y : ps.x, sy = c.kbi ? -ps.x : ps.y;
+    q = fma(lamx, sx, fma(lamy, sy, q));
+  } else if (IPK == 3) {
+    z.x = fma(lamx, ps.x, fma(lamy, ps.y, z.x));
+    z.y = fma(lamx, ps.y, fma(-lamy, ps.x, z.y));
+    z2.x = fma(lamx, v.x, fma(lamy, v.y, z2.x));
+    z2.y = fma(lamx, v.y, fma(-lamy, v.x, z2.y));
+  }
 }
 
-// One Pauli-form operator on register tile `v` (optionally fused with the
-// generator inner product against `l`).  XR: register part of the flip mask.
-template <int R, int XR, bool ROT, int IPK>
-__device__ __forceinline__ void pauli_step(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
-                                           uint32_t tbase, int sb, double2& z, double2& z2) {
+// Apply one op to register tile v; SHAPE: RS_DIAG / RS_LANE / RS_REG (flip bit XB).
+// For IPK != 0, `l` is lambda (read only) and the inner product uses the
+// pre-update v (phi_{i+1}).
+template <int R, int SHAPE, int XB, int IPK, bool CTRL>
+__device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[1 << R], const OpCtx& c,
+                                       uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
   constexpr int NR = 1 << R;
-  constexpr int LOW = XR & -XR;
-  const uint32_t xl = op.x & 31u;
-  const bool bi = (op.flags & RF_BI) != 0;
-  const double2 a = op.a, b = op.b;
+  constexpr int XR = (SHAPE == RS_REG) ? (1 << XB) : 0;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
-    if (XR != 0 && (j & LOW)) continue;  // handled with its pair's low member
+    if (XR != 0 && (j & XR)) continue;  // register pairs handled at the low member
     const int jp = j ^ XR;
-    const uint32_t tj = tbase | (uint32_t(j) << 5);
-    double2 pj = v[jp];
-    double2 pjp = v[j];
-    if (xl) {
-      pj = shfl2(pj, xl);
-      if (XR != 0) pjp = shfl2(pjp, xl);
+    double2 pj = v[jp];  // partner of slot j
+    double2 pp = v[j];   // partner of slot jp (register pairs)
+    if (SHAPE == RS_LANE) pj = shfl2(pj, xl);
+    const uint32_t sj = ((c.smask >> j) & 1u) ^ c.slw;
+    const double2 psj = sflip(pj, sj);
+    const bool okj = !CTRL || (c.clw_ok && ((c.cmask >> j) & 1u));
+    double& q = (j & 1) ? q1 : q0;  // two chains for the reduction
+    if (IPK != 0) {
+      if (!CTRL || okj) ip_term<IPK>(c, l[j].x, l[j].y, psj, v[j], q, z, z2);
     }
-    const int sj = par32((tj ^ op.x) & op.z) ^ sb;
-    const bool okj = (tj & op.c) == op.c;
-    if (okj) accumulate<IPK>(z, z2, l[j], pj, v[j], sj);
-    const double2 nj = okj ? combine<ROT>(a, b, bi, v[j], pj, sj) : v[j];
+    const double2 nj = upd(c, v[j], psj);
     if (XR != 0) {
-      const uint32_t tp = tbase | (uint32_t(jp) << 5);
-      const int sp = par32((tp ^ op.x) & op.z) ^ sb;
-      if (okj) accumulate<IPK>(z, z2, l[jp], pjp, v[jp], sp);
-      v[jp] = okj ? combine<ROT>(a, b, bi, v[jp], pjp, sp) : v[jp];
+      const uint32_t sp = ((c.smask >> jp) & 1u) ^ c.slw;
+      const double2 psp = sflip(pp, sp);
+      if (IPK != 0) {
+        if (!CTRL || okj) ip_term<IPK>(c, l[jp].x, l[jp].y, psp, v[jp], q1, z, z2);
+      }
+      const double2 np = upd(c, v[jp], psp);
+      v[jp] = (!CTRL || okj) ? np : v[jp];
     }
-    v[j] = nj;
+    v[j] = (!CTRL || okj) ? nj : v[j];
   }
 }
 
-template <int R, bool ROT, int IPK>
-__device__ __forceinline__ void pauli_dispatch(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
-                                               uint32_t tbase, int sb, double2& z, double2& z2) {
-  const uint32_t xr = (op.x >> 5) & ((1u << R) - 1u);
-  switch (xr) {
-#define SVGB_XR(N)                                                        \
-  case N:                                                                 \
-    if constexpr (N < (1 << R)) pauli_step<R, N, ROT, IPK>(v, l, op, tbase, sb, z, z2); \
-    break;
-    SVGB_XR(0) SVGB_XR(1) SVGB_XR(2) SVGB_XR(3) SVGB_XR(4) SVGB_XR(5) SVGB_XR(6) SVGB_XR(7)
-    SVGB_XR(8) SVGB_XR(9) SVGB_XR(10) SVGB_XR(11) SVGB_XR(12) SVGB_XR(13) SVGB_XR(14) SVGB_XR(15)
-#undef SVGB_XR
-    default:
-      break;
+template <int R, int IPK, bool CTRL>
+__device__ __forceinline__ void reg_op_shape(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
+                                             const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
+  if (op.shape == RS_DIAG) {
+    reg_op<R, RS_DIAG, 0, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2);
+  } else if (op.shape == RS_LANE) {
+    reg_op<R, RS_LANE, 0, IPK, CTRL>(v, l, c, op.xl, q0, q1, z, z2);
+  } else {
+    switch (op.xr) {
+      case 1: reg_op<R, RS_REG, 0, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      case 2: reg_op<R, RS_REG, 1, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      case 4: reg_op<R, RS_REG, 2, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      default:
+        if constexpr (R > 3) reg_op<R, RS_REG, 3, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2);
+        break;
+    }
   }
 }
 
 template <int R, int IPK>
-__device__ __forceinline__ void pauli_op(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
-                                         uint32_t tbase, int sb, double2& z, double2& z2) {
-  if (op.flags & RF_ROT)
-    pauli_dispatch<R, true, IPK>(v, l, op, tbase, sb, z, z2);
+__device__ __forceinline__ void reg_op_any(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
+                                           const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
+  if (op.flags & RF_CTRL)
+    reg_op_shape<R, IPK, true>(v, l, op, c, q0, q1, z, z2);
   else
-    pauli_dispatch<R, false, IPK>(v, l, op, tbase, sb, z, z2);
+    reg_op_shape<R, IPK, false>(v, l, op, c, q0, q1, z, z2);
+}
+
+__device__ __forceinline__ double warp_sum1(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
 }
 
 }  // namespace
 
 template <int R, int NB>
-__global__ void __launch_bounds__(256, 1) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
-                                                  const PassDesc d, const SegDesc* __restrict__ segs,
-                                                  const RegOp* __restrict__ rops, const DevOp* __restrict__ ops,
-                                                  const double2* __restrict__ coef,
-                                                  double2* __restrict__ partials) {
+__global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
+                                                             const PassDesc d, const SegDesc* __restrict__ segs,
+                                                             const RegOp* __restrict__ rops,
+                                                             const DevOp* __restrict__ ops,
+                                                             const double2* __restrict__ coef,
+                                                             double2* __restrict__ partials) {
   constexpr int NR = 1 << R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint8_t sq[kMaxQubits];
@@ -227,32 +254,40 @@ __global__ void __launch_bounds__(256, 1) k_pass_reg(double2* __restrict__ b0, d
           if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
           in_smem = false;
         }
+        RegOp nxt = rops[sg.op_begin];
         for (int o = sg.op_begin; o < sg.op_end; ++o) {
-          const RegOp op = rops[o];
+          const RegOp op = nxt;
+          if (o + 1 < sg.op_end) nxt = rops[o + 1];
           if ((base & op.co) != op.co) continue;
-          const int sb = par64(base & op.zo);
+          OpCtx c;
+          c.a = op.a;
+          c.bb = op.bb;
+          c.slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(base & op.zo)) & 1u;
+          c.smask = op.smask;
+          c.cmask = op.cmask;
+          c.clw_ok = (tbase & op.clw) == op.clw;
+          c.bi = (op.flags & RF_BI) != 0;
+          c.kbi = (op.flags & RF_KBI) != 0;
+          double q0 = 0.0, q1 = 0.0;
           double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
           if (op.kind == ROP_LAM) {
-            if constexpr (NB == 2) pauli_op<R, 0>(l, v, op, tbase, sb, z, z2);
-          } else if (NB == 1 || !(op.flags & RF_IP)) {
-            pauli_op<R, 0>(v, l, op, tbase, sb, z, z2);
+            if constexpr (NB == 2) reg_op_any<R, 0>(l, v, op, c, q0, q1, z, z2);
+          } else if (NB == 1 || !(op.flags & (RF_IP1 | RF_IP3))) {
+            reg_op_any<R, 0>(v, l, op, c, q0, q1, z, z2);
           } else if constexpr (NB == 2) {
-            const uint32_t ipk = (op.flags >> 1) & 3u;
-            if (op.flags & RF_IP_DIAG) {
-              pauli_op<R, 3>(v, l, op, tbase, sb, z, z2);
-            } else if (ipk == 1) {
-              pauli_op<R, 1>(v, l, op, tbase, sb, z, z2);
-            } else if (ipk == 2) {
-              pauli_op<R, 2>(v, l, op, tbase, sb, z, z2);
+            double2 contrib;
+            if (op.flags & RF_IP1) {
+              reg_op_any<R, 1>(v, l, op, c, q0, q1, z, z2);
+              contrib = make_double2(op.kr * warp_sum1(q0 + q1), 0.0);
             } else {
-              pauli_op<R, 3>(v, l, op, tbase, sb, z, z2);
+              reg_op_any<R, 3>(v, l, op, c, q0, q1, z, z2);
+              z = warp_sum(z);
+              z2 = warp_sum(z2);
+              contrib = cfma(op.kb, z, cmul(op.ka, z2));
             }
-            z = warp_sum(z);
-            z2 = warp_sum(z2);
             if (lane == 0) {
-              const double2 c = cfma(op.kb, z, cmul(op.ka, z2));
               double2& acc = wacc[warp * d.nslots + op.slot];
-              acc = make_double2(acc.x + c.x, acc.y + c.y);
+              acc = make_double2(acc.x + contrib.x, acc.y + contrib.y);
             }
           }
         }
@@ -307,6 +342,8 @@ template __global__ void k_pass_reg<kRegBits, 2>(double2*, double2*, const PassD
 size_t reg_smem(int k, int nb, int nwarps, int nslots, bool tiles) {
   return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0));
 }
+
+int reg_max_threads() { return kRegThreads; }
 
 static cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
   cudaFuncAttributes attr;
