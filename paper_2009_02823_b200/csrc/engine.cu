@@ -358,23 +358,31 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
   const double2 ph = ipow(g.n_y);
   const double2 b = cm(d2(c[1]), ph);
   op.a = c[0].re;
-  if (b.x == 0.0 && b.y != 0.0) {
-    op.flags |= RF_BI;
-    op.bb = b.y;
-  } else {
-    op.bb = b.x;
+  // BI: b' imaginary.  With b' == 0 either form works; pick the generator's
+  // so the fused inner product can use the same compile-time variant.
+  bool bi = b.x == 0.0 && b.y != 0.0;
+  double2 kb = make_double2(0.0, 0.0), ka = kb;
+  if (kpost) {
+    ka = d2(kpost[0]);
+    kb = cm(d2(kpost[1]), ph);
+    if (b.x == 0.0 && b.y == 0.0) bi = kb.x == 0.0 && kb.y != 0.0;
   }
+  if (bi) op.flags |= RF_BI;
+  op.bb = bi ? b.y : b.x;
   if (kpost) {
     op.slot = slot;
-    op.ka = d2(kpost[0]);
-    op.kb = cm(d2(kpost[1]), ph);
-    const bool diag = op.ka.x != 0.0 || op.ka.y != 0.0;
-    if (real_sums && !diag && op.kb.y == 0.0) {
+    op.ka = ka;
+    op.kb = kb;
+    const bool diag = ka.x != 0.0 || ka.y != 0.0;
+    // single-component inner product when only Re(sums) is needed and kb' is
+    // real (Re(kb' z) = kb'.x Re z) or imaginary (Re(i k z) = -k Im z) --
+    // the latter must coincide with the update's BI variant.
+    if (real_sums && !diag && kb.y == 0.0 && !bi) {
       op.flags |= RF_IP1;
-      op.kr = op.kb.x;  // Re(kb' z) = kb'.x Re(z)
-    } else if (real_sums && !diag && op.kb.x == 0.0) {
+      op.kr = kb.x;
+    } else if (real_sums && !diag && kb.x == 0.0 && bi) {
       op.flags |= RF_IP1 | RF_KBI;
-      op.kr = -op.kb.y;  // Re(i kappa z) = -kappa Im(z)
+      op.kr = -kb.y;
     } else {
       op.flags |= RF_IP3;
     }
@@ -446,6 +454,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     l.nb = nb;
     l.threads = 32 << wbits;
     l.d.seg_begin = static_cast<int>(L.segs.size());
+    l.d.op_begin = static_cast<int>(L.rops.size());  // this pass's register ops (staged in smem)
     return l;
   };
   // default register layout for shared-memory segments: lowest non-lane positions
@@ -487,6 +496,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         L.segs.push_back(sd);
       }
       l.d.seg_end = static_cast<int>(L.segs.size());
+      l.d.op_end = static_cast<int>(L.rops.size());
       if (psegs[pi].size() > 1) l.tiles = true;
       L.fwd.push_back(l);
     }
@@ -594,6 +604,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
           L.segs.push_back(sd);
         }
         l.d.seg_end = static_cast<int>(L.segs.size());
+        l.d.op_end = static_cast<int>(L.rops.size());
         if (sgs.size() > 1) l.tiles = true;
         l.d.nslots = static_cast<int>(slot);
         L.rev.push_back(l);
@@ -619,7 +630,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         l.grid = clamp_grid(occupancy(2, l.smem));
         break;
       case L_REG:
-        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.tiles);
+        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles);
         l.grid = clamp_grid(reg_occupancy(l.nb, l.threads, l.smem));
         break;
       case L_OBS:

@@ -106,26 +106,32 @@ __device__ __forceinline__ void from_smem(double2 (&v)[1 << R], const double2* s
 
 // Per-op, per-thread constants.
 struct OpCtx {
-  double a, bb;
-  uint32_t slw;   // lane/warp/base part of the partner sign (0/1)
+  double a, bb;    // BI: new = a v + i bb ps ; else new = a v + bb ps
+  double2 bc;      // IPK 3 (generic): b' as a complex number
+  uint32_t slw;    // lane/warp/base part of the partner sign (0/1)
   uint32_t smask, cmask;
-  bool clw_ok;    // lane/warp part of the control test
-  bool bi, kbi;
+  bool clw_ok;     // lane/warp part of the control test
 };
 
-// One amplitude: v <- a v + bb * (i^BI) * p_signed   (p_signed already carries the sign)
+// One amplitude: v <- a v + b' ps   (ps already carries the partner sign)
+template <int BI>
 __device__ __forceinline__ double2 upd(const OpCtx& c, double2 v, double2 ps) {
-  const double px = c.bi ? -ps.y : ps.x, py = c.bi ? ps.x : ps.y;
-  return make_double2(fma(c.bb, px, c.a * v.x), fma(c.bb, py, c.a * v.y));
+  if (BI == 1) return make_double2(fma(-c.bb, ps.y, c.a * v.x), fma(c.bb, ps.x, c.a * v.y));
+  if (BI == 0) return make_double2(fma(c.bb, ps.x, c.a * v.x), fma(c.bb, ps.y, c.a * v.y));
+  return make_double2(fma(c.bc.x, ps.x, fma(-c.bc.y, ps.y, c.a * v.x)),
+                      fma(c.bc.x, ps.y, fma(c.bc.y, ps.x, c.a * v.y)));  // generic complex b'
 }
 
 // Inner-product terms for one amplitude with signed partner ps.
-template <int IPK>
-__device__ __forceinline__ void ip_term(const OpCtx& c, double lamx, double lamy, double2 ps, double2 v, double& q,
-                                        double2& z, double2& z2) {
-  if (IPK == 1) {  // q += Re(conj(lam) * sel(ps)), sel = identity or -i
-    const double sx = c.kbi ? ps.y : ps.x, sy = c.kbi ? -ps.x : ps.y;
-    q = fma(lamx, sx, fma(lamy, sy, q));
+// IPK 1: q += Re(conj(lam) sel(ps)) with sel = -i (BI: Im part) or 1 ; IPK 3: full z, z2.
+template <int IPK, int BI>
+__device__ __forceinline__ void ip_term(double lamx, double lamy, double2 ps, double2 v, double& q, double2& z,
+                                        double2& z2) {
+  if (IPK == 1) {
+    if (BI == 1)
+      q = fma(lamx, ps.y, fma(-lamy, ps.x, q));
+    else
+      q = fma(lamx, ps.x, fma(lamy, ps.y, q));
   } else if (IPK == 3) {
     z.x = fma(lamx, ps.x, fma(lamy, ps.y, z.x));
     z.y = fma(lamx, ps.y, fma(-lamy, ps.x, z.y));
@@ -136,8 +142,8 @@ __device__ __forceinline__ void ip_term(const OpCtx& c, double lamx, double lamy
 
 // Apply one op to register tile v; SHAPE: RS_DIAG / RS_LANE / RS_REG (flip bit XB).
 // For IPK != 0, `l` is lambda (read only) and the inner product uses the
-// pre-update v (phi_{i+1}).
-template <int R, int SHAPE, int XB, int IPK, bool CTRL>
+// pre-update v (phi_{i+1}).  BI: 0/1 = real/imaginary b' (and generator), 2 = generic.
+template <int R, int SHAPE, int XB, int IPK, int BI, bool CTRL>
 __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[1 << R], const OpCtx& c,
                                        uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
   constexpr int NR = 1 << R;
@@ -147,43 +153,35 @@ __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[
     if (XR != 0 && (j & XR)) continue;  // register pairs handled at the low member
     const int jp = j ^ XR;
     double2 pj = v[jp];  // partner of slot j
-    double2 pp = v[j];   // partner of slot jp (register pairs)
     if (SHAPE == RS_LANE) pj = shfl2(pj, xl);
-    const uint32_t sj = ((c.smask >> j) & 1u) ^ c.slw;
-    const double2 psj = sflip(pj, sj);
+    const double2 psj = sflip(pj, ((c.smask >> j) & 1u) ^ c.slw);
     const bool okj = !CTRL || (c.clw_ok && ((c.cmask >> j) & 1u));
-    double& q = (j & 1) ? q1 : q0;  // two chains for the reduction
-    if (IPK != 0) {
-      if (!CTRL || okj) ip_term<IPK>(c, l[j].x, l[j].y, psj, v[j], q, z, z2);
-    }
-    const double2 nj = upd(c, v[j], psj);
+    if (IPK != 0 && okj) ip_term<IPK, BI>(l[j].x, l[j].y, psj, v[j], (j & 1) ? q1 : q0, z, z2);
+    const double2 nj = upd<BI>(c, v[j], psj);
     if (XR != 0) {
-      const uint32_t sp = ((c.smask >> jp) & 1u) ^ c.slw;
-      const double2 psp = sflip(pp, sp);
-      if (IPK != 0) {
-        if (!CTRL || okj) ip_term<IPK>(c, l[jp].x, l[jp].y, psp, v[jp], q1, z, z2);
-      }
-      const double2 np = upd(c, v[jp], psp);
-      v[jp] = (!CTRL || okj) ? np : v[jp];
+      const double2 psp = sflip(v[j], ((c.smask >> jp) & 1u) ^ c.slw);
+      if (IPK != 0 && okj) ip_term<IPK, BI>(l[jp].x, l[jp].y, psp, v[jp], q1, z, z2);
+      const double2 np = upd<BI>(c, v[jp], psp);
+      if (!CTRL || okj) v[jp] = np;
     }
-    v[j] = (!CTRL || okj) ? nj : v[j];
+    if (!CTRL || okj) v[j] = nj;
   }
 }
 
-template <int R, int IPK, bool CTRL>
+template <int R, int IPK, int BI, bool CTRL>
 __device__ __forceinline__ void reg_op_shape(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
                                              const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
   if (op.shape == RS_DIAG) {
-    reg_op<R, RS_DIAG, 0, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2);
+    reg_op<R, RS_DIAG, 0, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2);
   } else if (op.shape == RS_LANE) {
-    reg_op<R, RS_LANE, 0, IPK, CTRL>(v, l, c, op.xl, q0, q1, z, z2);
+    reg_op<R, RS_LANE, 0, IPK, BI, CTRL>(v, l, c, op.xl, q0, q1, z, z2);
   } else {
     switch (op.xr) {
-      case 1: reg_op<R, RS_REG, 0, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
-      case 2: reg_op<R, RS_REG, 1, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
-      case 4: reg_op<R, RS_REG, 2, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      case 1: reg_op<R, RS_REG, 0, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      case 2: reg_op<R, RS_REG, 1, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      case 4: reg_op<R, RS_REG, 2, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
       default:
-        if constexpr (R > 3) reg_op<R, RS_REG, 3, IPK, CTRL>(v, l, c, 0, q0, q1, z, z2);
+        if constexpr (R > 3) reg_op<R, RS_REG, 3, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2);
         break;
     }
   }
@@ -192,10 +190,23 @@ __device__ __forceinline__ void reg_op_shape(double2 (&v)[1 << R], const double2
 template <int R, int IPK>
 __device__ __forceinline__ void reg_op_any(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
                                            const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
-  if (op.flags & RF_CTRL)
-    reg_op_shape<R, IPK, true>(v, l, op, c, q0, q1, z, z2);
-  else
-    reg_op_shape<R, IPK, false>(v, l, op, c, q0, q1, z, z2);
+  const bool ctrl = (op.flags & RF_CTRL) != 0;
+  if (IPK == 3) {  // complex generator path (non-Hermitian sweeps): generic b'
+    if (ctrl)
+      reg_op_shape<R, 3, 2, true>(v, l, op, c, q0, q1, z, z2);
+    else
+      reg_op_shape<R, 3, 2, false>(v, l, op, c, q0, q1, z, z2);
+  } else if (op.flags & RF_BI) {
+    if (ctrl)
+      reg_op_shape<R, IPK, 1, true>(v, l, op, c, q0, q1, z, z2);
+    else
+      reg_op_shape<R, IPK, 1, false>(v, l, op, c, q0, q1, z, z2);
+  } else {
+    if (ctrl)
+      reg_op_shape<R, IPK, 0, true>(v, l, op, c, q0, q1, z, z2);
+    else
+      reg_op_shape<R, IPK, 0, false>(v, l, op, c, q0, q1, z, z2);
+  }
 }
 
 __device__ __forceinline__ double warp_sum1(double v) {
@@ -207,7 +218,7 @@ __device__ __forceinline__ double warp_sum1(double v) {
 }  // namespace
 
 template <int R, int NB>
-__global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
+__global__ void __launch_bounds__(kRegThreads, NB == 1 ? 3 : 2) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
                                                              const PassDesc d, const SegDesc* __restrict__ segs,
                                                              const RegOp* __restrict__ rops,
                                                              const DevOp* __restrict__ ops,
@@ -221,9 +232,16 @@ __global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wbits = d.k - 5 - R;
   double2* wacc = reinterpret_cast<double2*>(smem_raw);  // [nwarps][nslots]
-  double2* st0 = wacc + nwarps * d.nslots;                // shared tiles (multi-segment passes)
+  RegOp* sops = reinterpret_cast<RegOp*>(wacc + nwarps * d.nslots);  // this pass's register ops
+  const int nops = d.op_end - d.op_begin;
+  double2* st0 = reinterpret_cast<double2*>(sops + nops);  // shared tiles (multi-segment passes)
   double2* st1 = st0 + (1u << d.k);
   for (int i = threadIdx.x; i < nwarps * d.nslots; i += nthr) wacc[i] = make_double2(0.0, 0.0);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(rops + d.op_begin);
+    uint4* dst = reinterpret_cast<uint4*>(sops);
+    for (int i = threadIdx.x; i < nops * int(sizeof(RegOp) / 16); i += nthr) dst[i] = src[i];
+  }
   if (threadIdx.x < kMaxQubits) sq[threadIdx.x] = d.q[threadIdx.x];
   __syncthreads();
 
@@ -254,20 +272,17 @@ __global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict
           if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
           in_smem = false;
         }
-        RegOp nxt = rops[sg.op_begin];
-        for (int o = sg.op_begin; o < sg.op_end; ++o) {
-          const RegOp op = nxt;
-          if (o + 1 < sg.op_end) nxt = rops[o + 1];
+        for (int o = sg.op_begin - d.op_begin; o < sg.op_end - d.op_begin; ++o) {
+          const RegOp& op = sops[o];
           if ((base & op.co) != op.co) continue;
           OpCtx c;
           c.a = op.a;
           c.bb = op.bb;
+          c.bc = (op.flags & RF_BI) ? make_double2(0.0, op.bb) : make_double2(op.bb, 0.0);
           c.slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(base & op.zo)) & 1u;
           c.smask = op.smask;
           c.cmask = op.cmask;
           c.clw_ok = (tbase & op.clw) == op.clw;
-          c.bi = (op.flags & RF_BI) != 0;
-          c.kbi = (op.flags & RF_KBI) != 0;
           double q0 = 0.0, q1 = 0.0;
           double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
           if (op.kind == ROP_LAM) {
@@ -339,8 +354,8 @@ template __global__ void k_pass_reg<kRegBits, 1>(double2*, double2*, const PassD
 template __global__ void k_pass_reg<kRegBits, 2>(double2*, double2*, const PassDesc, const SegDesc*, const RegOp*,
                                                  const DevOp*, const double2*, double2*);
 
-size_t reg_smem(int k, int nb, int nwarps, int nslots, bool tiles) {
-  return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0));
+size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles) {
+  return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(RegOp) * nops;
 }
 
 int reg_max_threads() { return kRegThreads; }
