@@ -8,7 +8,7 @@ namespace svgb {
 constexpr int kMaxQubits = 40;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRegBits = 4;  // amplitudes per thread per buffer = 2^kRegBits (register-tile passes)
+constexpr int kRegBits = 3;  // amplitudes per thread per buffer = 2^kRegBits (register-tile passes)
 
 enum OpKind : uint32_t {
   OP_APPLY_PAULI = 0,  // buf <- a*buf + b'*Psign buf          (b' = b * i^{n_y})

@@ -28,7 +28,7 @@ namespace svgb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kRegThreads = 128;  // launch bound: k = 11 tiles (4 warps)
+constexpr int kRegThreads = 256;  // launch bound: k = 11 tiles with R = 3 (8 warps)
 
 __device__ __forceinline__ double2 shfl2(double2 v, uint32_t m) {
   return make_double2(__shfl_xor_sync(kFull, v.x, m), __shfl_xor_sync(kFull, v.y, m));
@@ -143,7 +143,9 @@ __device__ __forceinline__ void ip_term(double lamx, double lamy, double2 ps, do
 // Apply one op to register tile v; SHAPE: RS_DIAG / RS_LANE / RS_REG (flip bit XB).
 // For IPK != 0, `l` is lambda (read only) and the inner product uses the
 // pre-update v (phi_{i+1}).  BI: 0/1 = real/imaginary b' (and generator), 2 = generic.
-template <int R, int SHAPE, int XB, int IPK, int BI, bool CTRL>
+// SIGNED: the partner sign varies with the register slot (smask != 0);
+// otherwise it is uniform per op and was folded into the coefficients.
+template <int R, int SHAPE, int XB, int IPK, int BI, bool CTRL, bool SIGNED>
 __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[1 << R], const OpCtx& c,
                                        uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
   constexpr int NR = 1 << R;
@@ -154,12 +156,12 @@ __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[
     const int jp = j ^ XR;
     double2 pj = v[jp];  // partner of slot j
     if (SHAPE == RS_LANE) pj = shfl2(pj, xl);
-    const double2 psj = sflip(pj, ((c.smask >> j) & 1u) ^ c.slw);
+    const double2 psj = SIGNED ? sflip(pj, ((c.smask >> j) & 1u) ^ c.slw) : pj;
     const bool okj = !CTRL || (c.clw_ok && ((c.cmask >> j) & 1u));
     if (IPK != 0 && okj) ip_term<IPK, BI>(l[j].x, l[j].y, psj, v[j], (j & 1) ? q1 : q0, z, z2);
     const double2 nj = upd<BI>(c, v[j], psj);
     if (XR != 0) {
-      const double2 psp = sflip(v[j], ((c.smask >> jp) & 1u) ^ c.slw);
+      const double2 psp = SIGNED ? sflip(v[j], ((c.smask >> jp) & 1u) ^ c.slw) : v[j];
       if (IPK != 0 && okj) ip_term<IPK, BI>(l[jp].x, l[jp].y, psp, v[jp], q1, z, z2);
       const double2 np = upd<BI>(c, v[jp], psp);
       if (!CTRL || okj) v[jp] = np;
@@ -168,23 +170,32 @@ __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[
   }
 }
 
-template <int R, int IPK, int BI, bool CTRL>
+template <int R, int IPK, int BI, bool CTRL, bool SIGNED>
 __device__ __forceinline__ void reg_op_shape(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
                                              const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
   if (op.shape == RS_DIAG) {
-    reg_op<R, RS_DIAG, 0, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2);
+    reg_op<R, RS_DIAG, 0, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2);
   } else if (op.shape == RS_LANE) {
-    reg_op<R, RS_LANE, 0, IPK, BI, CTRL>(v, l, c, op.xl, q0, q1, z, z2);
+    reg_op<R, RS_LANE, 0, IPK, BI, CTRL, SIGNED>(v, l, c, op.xl, q0, q1, z, z2);
   } else {
     switch (op.xr) {
-      case 1: reg_op<R, RS_REG, 0, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
-      case 2: reg_op<R, RS_REG, 1, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
-      case 4: reg_op<R, RS_REG, 2, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2); break;
+      case 1: reg_op<R, RS_REG, 0, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2); break;
+      case 2: reg_op<R, RS_REG, 1, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2); break;
+      case 4: reg_op<R, RS_REG, 2, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2); break;
       default:
-        if constexpr (R > 3) reg_op<R, RS_REG, 3, IPK, BI, CTRL>(v, l, c, 0, q0, q1, z, z2);
+        if constexpr (R > 3) reg_op<R, RS_REG, 3, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2);
         break;
     }
   }
+}
+
+template <int R, int IPK, int BI, bool CTRL>
+__device__ __forceinline__ void reg_op_sign(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
+                                            const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
+  if (op.smask != 0)
+    reg_op_shape<R, IPK, BI, CTRL, true>(v, l, op, c, q0, q1, z, z2);
+  else
+    reg_op_shape<R, IPK, BI, CTRL, false>(v, l, op, c, q0, q1, z, z2);
 }
 
 template <int R, int IPK>
@@ -193,19 +204,19 @@ __device__ __forceinline__ void reg_op_any(double2 (&v)[1 << R], const double2 (
   const bool ctrl = (op.flags & RF_CTRL) != 0;
   if (IPK == 3) {  // complex generator path (non-Hermitian sweeps): generic b'
     if (ctrl)
-      reg_op_shape<R, 3, 2, true>(v, l, op, c, q0, q1, z, z2);
+      reg_op_sign<R, 3, 2, true>(v, l, op, c, q0, q1, z, z2);
     else
-      reg_op_shape<R, 3, 2, false>(v, l, op, c, q0, q1, z, z2);
+      reg_op_sign<R, 3, 2, false>(v, l, op, c, q0, q1, z, z2);
   } else if (op.flags & RF_BI) {
     if (ctrl)
-      reg_op_shape<R, IPK, 1, true>(v, l, op, c, q0, q1, z, z2);
+      reg_op_sign<R, IPK, 1, true>(v, l, op, c, q0, q1, z, z2);
     else
-      reg_op_shape<R, IPK, 1, false>(v, l, op, c, q0, q1, z, z2);
+      reg_op_sign<R, IPK, 1, false>(v, l, op, c, q0, q1, z, z2);
   } else {
     if (ctrl)
-      reg_op_shape<R, IPK, 0, true>(v, l, op, c, q0, q1, z, z2);
+      reg_op_sign<R, IPK, 0, true>(v, l, op, c, q0, q1, z, z2);
     else
-      reg_op_shape<R, IPK, 0, false>(v, l, op, c, q0, q1, z, z2);
+      reg_op_sign<R, IPK, 0, false>(v, l, op, c, q0, q1, z, z2);
   }
 }
 
@@ -218,7 +229,7 @@ __device__ __forceinline__ double warp_sum1(double v) {
 }  // namespace
 
 template <int R, int NB>
-__global__ void __launch_bounds__(kRegThreads, NB == 1 ? 3 : 2) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
+__global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
                                                              const PassDesc d, const SegDesc* __restrict__ segs,
                                                              const RegOp* __restrict__ rops,
                                                              const DevOp* __restrict__ ops,
@@ -283,6 +294,12 @@ __global__ void __launch_bounds__(kRegThreads, NB == 1 ? 3 : 2) k_pass_reg(doubl
           c.smask = op.smask;
           c.cmask = op.cmask;
           c.clw_ok = (tbase & op.clw) == op.clw;
+          // uniform partner sign: fold into the coefficient (and into the IP result below)
+          const bool fold = op.smask == 0 && c.slw;
+          if (fold) {
+            c.bb = -c.bb;
+            c.bc = make_double2(-c.bc.x, -c.bc.y);
+          }
           double q0 = 0.0, q1 = 0.0;
           double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
           if (op.kind == ROP_LAM) {
@@ -293,9 +310,11 @@ __global__ void __launch_bounds__(kRegThreads, NB == 1 ? 3 : 2) k_pass_reg(doubl
             double2 contrib;
             if (op.flags & RF_IP1) {
               reg_op_any<R, 1>(v, l, op, c, q0, q1, z, z2);
-              contrib = make_double2(op.kr * warp_sum1(q0 + q1), 0.0);
+              const double q = fold ? -(q0 + q1) : q0 + q1;
+              contrib = make_double2(op.kr * warp_sum1(q), 0.0);
             } else {
               reg_op_any<R, 3>(v, l, op, c, q0, q1, z, z2);
+              if (fold) z = make_double2(-z.x, -z.y);
               z = warp_sum(z);
               z2 = warp_sum(z2);
               contrib = cfma(op.kb, z, cmul(op.ka, z2));
