@@ -77,9 +77,9 @@ struct PassDesc {
 // register part of t is precomputed per register slot (smask), so the device
 // only adds the lane/warp part.  Controls likewise (cmask + clw).
 enum RegOpKind : uint32_t {
-  ROP_FWD = 0,  // psi <- op psi                                     (forward)
-  ROP_REV = 1,  // [slot += <lam| K' |phi>]; phi <- op phi            (reverse: IP + rewind)
-  ROP_LAM = 2,  // lam <- op lam                                      (reverse: adjoint)
+  ROP_FWD = 0,  // psi <- op psi                                            (forward)
+  ROP_REV = 1,  // [slot += <lam| K' |phi>]; phi <- op phi; lam <- op lam    (reverse: for a
+                // unitary Pauli-form gate the rewind U^-1 and the adjoint U^dag coincide)
 };
 enum RegOpFlags : uint32_t {
   RF_IP1 = 1u,    // ROP_REV: accumulate one real component q = Re(conj(lam) sel(P phi))
@@ -95,7 +95,8 @@ enum RegOpShape : uint32_t {
 };
 
 struct RegOp {
-  uint32_t kind, flags, shape;
+  uint32_t variant;   // flat code-path id (kernels_reg.cu run_variant)
+  uint32_t flags, shape;
   uint32_t xl;        // lane flip mask
   uint32_t xr;        // register flip mask (one bit) for RS_REG
   uint32_t zlw;       // sign mask on lane | warp bits (segment-local)

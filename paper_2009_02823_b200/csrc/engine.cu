@@ -121,6 +121,7 @@ struct Launch {
 struct Lowered {
   int n = 0, k = 0, b = 0;
   bool reg = false;  // register-tile kernels in use
+  int R = 3;         // their register bits
   std::vector<DevOp> ops;
   std::vector<double2> coef;
   std::vector<DevTerm> terms;
@@ -148,7 +149,7 @@ struct svg_engine {
   size_t max_smem = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0;
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 3;
   DeviceBuf psi, lam, partials, blob, results;
   HostBuf hblob, hres;
   cudaEvent_t ev[6] = {};
@@ -304,6 +305,7 @@ Gen make_gen(const svg_gate& g, const svg_deriv& dv) {
 
 // Segment-local bit of each tile position for a register segment.
 struct SegLocal {
+  int R = 3;  // register bits of the segment layout
   uint8_t bit[32];
   uint32_t conv(uint32_t tile_mask) const {
     uint32_t r = 0;
@@ -312,7 +314,8 @@ struct SegLocal {
   }
 };
 
-SegDesc make_seg(int kind, uint32_t regmask, int k, SegLocal* sl) {
+SegDesc make_seg(int kind, uint32_t regmask, int k, int R, SegLocal* sl) {
+  sl->R = R;
   SegDesc sd;
   std::memset(&sd, 0, sizeof(sd));
   sd.kind = kind;
@@ -325,7 +328,7 @@ SegDesc make_seg(int kind, uint32_t regmask, int k, SegLocal* sl) {
       sl->bit[pos] = static_cast<uint8_t>(5 + r++);
     } else {
       sd.warppos[w] = static_cast<uint8_t>(pos);
-      sl->bit[pos] = static_cast<uint8_t>(5 + kRegBits + w++);
+      sl->bit[pos] = static_cast<uint8_t>(5 + R + w++);
     }
   }
   return sd;
@@ -337,8 +340,8 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
               const svg_c128* c, const svg_c128* kpost, uint32_t slot, bool real_sums) {
   RegOp op;
   std::memset(&op, 0, sizeof(op));
-  op.kind = kind;
-  const uint32_t regbits = ((1u << kRegBits) - 1u) << 5;
+  const int R = sl.R;
+  const uint32_t regbits = ((1u << R) - 1u) << 5;
   const uint32_t xloc = sl.conv(tm.local(g.x_mask));
   const uint32_t zloc = sl.conv(tm.local(g.z_mask));
   const uint32_t cloc = sl.conv(tm.local(g.ctrl_mask));
@@ -348,7 +351,7 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
   op.zlw = zloc & ~regbits;
   op.clw = cloc & ~regbits;
   const uint32_t zr = (zloc & regbits) >> 5, cr = (cloc & regbits) >> 5;
-  for (uint32_t j = 0; j < (1u << kRegBits); ++j) {
+  for (uint32_t j = 0; j < (1u << R); ++j) {
     op.smask |= static_cast<uint32_t>(__builtin_popcount((j ^ op.xr) & zr) & 1) << j;
     op.cmask |= static_cast<uint32_t>((j & cr) == cr) << j;
   }
@@ -387,6 +390,19 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
       op.flags |= RF_IP3;
     }
   }
+  // flat code-path id, see run_variant in kernels_reg.cu
+  const uint32_t nshape = 2 + R;
+  const uint32_t shape_id = op.shape == RS_DIAG ? 0 : op.shape == RS_LANE ? 1 : 2 + __builtin_ctz(op.xr);
+  uint32_t mode = bi ? 1 : 0;
+  if (kind == ROP_REV) {
+    if (op.flags & RF_IP3)
+      mode = 6;
+    else if (op.flags & RF_IP1)
+      mode = 4 + (bi ? 1 : 0);
+    else
+      mode = 2 + (bi ? 1 : 0);
+  }
+  op.variant = shape_id + nshape * ((op.smask != 0) + 2 * ((cloc != 0) + 2 * mode));
   L.rops.push_back(op);
 }
 
@@ -395,6 +411,8 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
 // touches lanes only or exactly one non-lane tile position.
 bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
   if (g.form != SVG_FORM_PAULI || g.nderiv > 1) return false;
+  for (int i = 0; i < 2; ++i)  // one reverse op serves phi and lambda: rewind must equal adjoint
+    if (g.rewind[i].re != g.adjoint[i].re || g.rewind[i].im != g.adjoint[i].im) return false;
   const double2 ph = ipow(g.n_y);
   for (const svg_c128* c : {g.fwd, g.rewind, g.adjoint}) {
     const double2 b = cm(d2(c[1]), ph);
@@ -412,9 +430,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   L.n = n;
   L.k = choose_tile_qubits(n, static_cast<int>(e->opt_tile), e->sms);
   L.b = (n <= L.k) ? n : std::min(5, L.k - 2);
-  const int wbits = L.k - 5 - kRegBits;
+  const int RB = static_cast<int>(e->opt_reg_bits);
+  L.R = RB;
+  const int wbits = L.k - 5 - RB;
   L.reg = e->opt_kernel != 1 && L.b >= 5 && wbits >= 0 && (32 << wbits) <= reg_max_threads();
-  if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 9..11 tile qubits");
+  if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 5 + reg_bits .. 13 tile qubits");
   PlanParams pp;
   pp.n = n;
   pp.k = L.k;
@@ -444,7 +464,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         flips[j] = tm.local(shapes[ps.items[j]].flip);
         dense[j] = !reg_capable(g, flips[j]);
       }
-      psegs[pi] = plan_segments(flips, dense, L.k, kRegBits);
+      psegs[pi] = plan_segments(flips, dense, L.k, RB);
     }
   }
   auto reg_launch = [&](const Pass& ps, int nb) {
@@ -458,7 +478,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     return l;
   };
   // default register layout for shared-memory segments: lowest non-lane positions
-  const uint32_t default_regs = ((1u << (5 + kRegBits)) - 1u) & ~31u;
+  const uint32_t default_regs = ((1u << (5 + RB)) - 1u) & ~31u;
 
   // forward passes
   for (size_t pi = 0; pi < gpasses.size(); ++pi) {
@@ -477,7 +497,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       uint32_t prev = ~0u;
       for (const Segment& sg : psegs[pi]) {
         SegLocal sl;
-        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, &sl);
+        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, RB, &sl);
         sd.same_map = sg.reg && sg.regmask == prev;
         prev = sg.reg ? sg.regmask : ~0u;
         if (sg.reg) {
@@ -577,7 +597,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
           const Segment& sg = *st;
           SegLocal sl;
-          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, &sl);
+          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, RB, &sl);
           sd.same_map = sg.reg && sg.regmask == prev;
           prev = sg.reg ? sg.regmask : ~0u;
           if (sg.reg) {
@@ -591,8 +611,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
                 deriv_slot[d] = {static_cast<int>(L.rev.size()), static_cast<int>(slot)};
                 kpost = gens[d].post;
               }
+              // one op rewinds phi AND lambda (rewind == adjoint for register-capable gates);
+              // the reference skips lambda's update at i = 0, whose value is never read again
               emit_rop(L, tm, sl, g, ROP_REV, g.rewind, kpost, kpost ? slot++ : 0, real_sums);
-              if (gi > 0) emit_rop(L, tm, sl, g, ROP_LAM, g.adjoint, nullptr, 0, real_sums);
             }
             sd.op_end = static_cast<int>(L.rops.size());
           } else {
@@ -631,7 +652,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         break;
       case L_REG:
         l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles);
-        l.grid = clamp_grid(reg_occupancy(l.nb, l.threads, l.smem));
+        l.grid = clamp_grid(reg_occupancy(l.nb, L.R, l.threads, l.smem));
         break;
       case L_OBS:
         l.smem = obs_smem(L.k, l.d.b);
@@ -754,7 +775,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     CK(cudaEventRecord(e->ev[1], s));
     for (const Launch& l : L.fwd) {
       if (l.kind == L_REG)
-        launch_pass_reg(1, l.d, l.grid, l.threads, l.smem, s, psi, nullptr, dsegs, drops, dops, dcoef, part);
+        launch_pass_reg(1, L.R, l.d, l.grid, l.threads, l.smem, s, psi, nullptr, dsegs, drops, dops, dcoef, part);
       else
         launch_fwd(l.d, l.grid, l.smem, s, psi, dops, dcoef);
     }
@@ -768,7 +789,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     CK(cudaEventRecord(e->ev[3], s));
     for (const Launch& l : L.rev) {
       if (l.kind == L_REG)
-        launch_pass_reg(2, l.d, l.grid, l.threads, l.smem, s, psi, lam, dsegs, drops, dops, dcoef, part);
+        launch_pass_reg(2, L.R, l.d, l.grid, l.threads, l.smem, s, psi, lam, dsegs, drops, dops, dcoef, part);
       else
         launch_rev(l.d, l.grid, l.smem, s, psi, lam, dops, dcoef, part);
     }
@@ -913,6 +934,9 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     e->opt_tile = value;
   } else if (k == "profile") {
     e->opt_profile = value;
+  } else if (k == "reg_bits") {
+    if (value != 3 && value != 4) return fail(SVG_EINVAL, "reg_bits must be 3 or 4");
+    e->opt_reg_bits = value;
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;

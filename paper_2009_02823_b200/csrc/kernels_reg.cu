@@ -145,80 +145,97 @@ __device__ __forceinline__ void ip_term(double lamx, double lamy, double2 ps, do
 // pre-update v (phi_{i+1}).  BI: 0/1 = real/imaginary b' (and generator), 2 = generic.
 // SIGNED: the partner sign varies with the register slot (smask != 0);
 // otherwise it is uniform per op and was folded into the coefficients.
-template <int R, int SHAPE, int XB, int IPK, int BI, bool CTRL, bool SIGNED>
-__device__ __forceinline__ void reg_op(double2 (&v)[1 << R], const double2 (&l)[1 << R], const OpCtx& c,
-                                       uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
+// DUAL: the same operator is also applied to the lambda tile `l` (reverse
+// pass: for a unitary Pauli-form gate the rewind R = U^-1 equals U^dag, so
+// phi and lambda share one op, its partner signs and its controls).
+template <int R, int SHAPE, int XB, int IPK, int BI, bool CTRL, bool SIGNED, bool DUAL>
+__device__ __forceinline__ void reg_op(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
+                                       double& q0, double& q1, double2& z, double2& z2) {
   constexpr int NR = 1 << R;
   constexpr int XR = (SHAPE == RS_REG) ? (1 << XB) : 0;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     if (XR != 0 && (j & XR)) continue;  // register pairs handled at the low member
     const int jp = j ^ XR;
-    double2 pj = v[jp];  // partner of slot j
-    if (SHAPE == RS_LANE) pj = shfl2(pj, xl);
-    const double2 psj = SIGNED ? sflip(pj, ((c.smask >> j) & 1u) ^ c.slw) : pj;
+    const uint32_t sj = SIGNED ? (((c.smask >> j) & 1u) ^ c.slw) : 0u;
+    const uint32_t sp = SIGNED ? (((c.smask >> jp) & 1u) ^ c.slw) : 0u;
     const bool okj = !CTRL || (c.clw_ok && ((c.cmask >> j) & 1u));
+    double2 pj = v[jp];  // partner of slot j (slot jp of the partner lane)
+    if (SHAPE == RS_LANE) pj = shfl2(pj, xl);
+    const double2 psj = SIGNED ? sflip(pj, sj) : pj;
+    double2 lpj = make_double2(0.0, 0.0);
+    if (DUAL) {
+      lpj = l[jp];
+      if (SHAPE == RS_LANE) lpj = shfl2(lpj, xl);
+      if (SIGNED) lpj = sflip(lpj, sj);
+    }
     if (IPK != 0 && okj) ip_term<IPK, BI>(l[j].x, l[j].y, psj, v[j], (j & 1) ? q1 : q0, z, z2);
     const double2 nj = upd<BI>(c, v[j], psj);
+    const double2 lnj = DUAL ? upd<BI>(c, l[j], lpj) : lpj;
     if (XR != 0) {
-      const double2 psp = SIGNED ? sflip(v[j], ((c.smask >> jp) & 1u) ^ c.slw) : v[j];
+      const double2 psp = SIGNED ? sflip(v[j], sp) : v[j];
       if (IPK != 0 && okj) ip_term<IPK, BI>(l[jp].x, l[jp].y, psp, v[jp], q1, z, z2);
       const double2 np = upd<BI>(c, v[jp], psp);
       if (!CTRL || okj) v[jp] = np;
+      if (DUAL) {
+        const double2 lnp = upd<BI>(c, l[jp], SIGNED ? sflip(l[j], sp) : l[j]);
+        if (!CTRL || okj) l[jp] = lnp;
+      }
     }
-    if (!CTRL || okj) v[j] = nj;
-  }
-}
-
-template <int R, int IPK, int BI, bool CTRL, bool SIGNED>
-__device__ __forceinline__ void reg_op_shape(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
-                                             const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
-  if (op.shape == RS_DIAG) {
-    reg_op<R, RS_DIAG, 0, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2);
-  } else if (op.shape == RS_LANE) {
-    reg_op<R, RS_LANE, 0, IPK, BI, CTRL, SIGNED>(v, l, c, op.xl, q0, q1, z, z2);
-  } else {
-    switch (op.xr) {
-      case 1: reg_op<R, RS_REG, 0, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2); break;
-      case 2: reg_op<R, RS_REG, 1, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2); break;
-      case 4: reg_op<R, RS_REG, 2, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2); break;
-      default:
-        if constexpr (R > 3) reg_op<R, RS_REG, 3, IPK, BI, CTRL, SIGNED>(v, l, c, 0, q0, q1, z, z2);
-        break;
+    if (!CTRL || okj) {
+      v[j] = nj;
+      if (DUAL) l[j] = lnj;
     }
   }
 }
 
-template <int R, int IPK, int BI, bool CTRL>
-__device__ __forceinline__ void reg_op_sign(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
-                                            const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
-  if (op.smask != 0)
-    reg_op_shape<R, IPK, BI, CTRL, true>(v, l, op, c, q0, q1, z, z2);
-  else
-    reg_op_shape<R, IPK, BI, CTRL, false>(v, l, op, c, q0, q1, z, z2);
-}
-
-template <int R, int IPK>
-__device__ __forceinline__ void reg_op_any(double2 (&v)[1 << R], const double2 (&l)[1 << R], const RegOp& op,
-                                           const OpCtx& c, double& q0, double& q1, double2& z, double2& z2) {
-  const bool ctrl = (op.flags & RF_CTRL) != 0;
-  if (IPK == 3) {  // complex generator path (non-Hermitian sweeps): generic b'
-    if (ctrl)
-      reg_op_sign<R, 3, 2, true>(v, l, op, c, q0, q1, z, z2);
-    else
-      reg_op_sign<R, 3, 2, false>(v, l, op, c, q0, q1, z, z2);
-  } else if (op.flags & RF_BI) {
-    if (ctrl)
-      reg_op_sign<R, IPK, 1, true>(v, l, op, c, q0, q1, z, z2);
-    else
-      reg_op_sign<R, IPK, 1, false>(v, l, op, c, q0, q1, z, z2);
-  } else {
-    if (ctrl)
-      reg_op_sign<R, IPK, 0, true>(v, l, op, c, q0, q1, z, z2);
-    else
-      reg_op_sign<R, IPK, 0, false>(v, l, op, c, q0, q1, z, z2);
+// Flat variant id (computed on the host, see engine.cu emit_rop):
+//   id = shape + NSHAPE * (signed + 2 * (ctrl + 2 * mode)),  NSHAPE = 2 + R
+//   shape: 0 diagonal, 1 lane flip, 2 + b register-bit-b flip
+//   mode:  0/1 forward (BI 0/1); 2/3 reverse IPK 0 (BI 0/1); 4/5 reverse IPK 1 (BI 0/1);
+//          6 reverse IPK 3 (generic complex coefficients)
+template <int R, int NB, int V>
+__device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
+                                            double& q0, double& q1, double2& z, double2& z2) {
+  constexpr int NSHAPE = 2 + R;
+  constexpr int NV = NSHAPE * 4 * 7;
+  if constexpr (V < NV) {
+    constexpr int shape = V % NSHAPE;
+    constexpr bool SIGNED = (V / NSHAPE) % 2;
+    constexpr bool CTRL = (V / NSHAPE / 2) % 2;
+    constexpr int mode = V / NSHAPE / 4;
+    constexpr int SH = shape == 0 ? RS_DIAG : (shape == 1 ? RS_LANE : RS_REG);
+    constexpr int XB = shape >= 2 ? shape - 2 : 0;
+    constexpr bool DUAL = mode >= 2;
+    constexpr int IPK = mode >= 6 ? 3 : (mode >= 4 ? 1 : 0);
+    constexpr int BI = mode == 6 ? 2 : (mode & 1);
+    if constexpr (NB == 2 || !DUAL) reg_op<R, SH, XB, IPK, BI, CTRL, SIGNED, DUAL>(v, l, c, xl, q0, q1, z, z2);
   }
 }
+
+#define SVGB_V1(N) \
+  case (N):        \
+    run_variant<R, NB, (N)>(v, l, c, xl, q0, q1, z, z2); \
+    break;
+#define SVGB_V4(N) SVGB_V1(N) SVGB_V1(N + 1) SVGB_V1(N + 2) SVGB_V1(N + 3)
+#define SVGB_V16(N) SVGB_V4(N) SVGB_V4(N + 4) SVGB_V4(N + 8) SVGB_V4(N + 12)
+#define SVGB_V64(N) SVGB_V16(N) SVGB_V16(N + 16) SVGB_V16(N + 32) SVGB_V16(N + 48)
+
+template <int R, int NB>
+__device__ __forceinline__ void dispatch(uint32_t id, double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c,
+                                         uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
+  switch (id) {
+    SVGB_V64(0)
+    SVGB_V64(64)
+    SVGB_V64(128)
+    default:
+      break;
+  }
+}
+#undef SVGB_V64
+#undef SVGB_V16
+#undef SVGB_V4
+#undef SVGB_V1
 
 __device__ __forceinline__ double warp_sum1(double v) {
 #pragma unroll
@@ -229,7 +246,7 @@ __device__ __forceinline__ double warp_sum1(double v) {
 }  // namespace
 
 template <int R, int NB>
-__global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
+__global__ void __launch_bounds__(kRegThreads, R == 3 ? 2 : 1) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
                                                              const PassDesc d, const SegDesc* __restrict__ segs,
                                                              const RegOp* __restrict__ rops,
                                                              const DevOp* __restrict__ ops,
@@ -302,18 +319,14 @@ __global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict
           }
           double q0 = 0.0, q1 = 0.0;
           double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
-          if (op.kind == ROP_LAM) {
-            if constexpr (NB == 2) reg_op_any<R, 0>(l, v, op, c, q0, q1, z, z2);
-          } else if (NB == 1 || !(op.flags & (RF_IP1 | RF_IP3))) {
-            reg_op_any<R, 0>(v, l, op, c, q0, q1, z, z2);
-          } else if constexpr (NB == 2) {
+          dispatch<R, NB>(op.variant, v, l, c, op.xl, q0, q1, z, z2);
+          if constexpr (NB == 2) {
+            if (!(op.flags & (RF_IP1 | RF_IP3))) continue;
             double2 contrib;
             if (op.flags & RF_IP1) {
-              reg_op_any<R, 1>(v, l, op, c, q0, q1, z, z2);
               const double q = fold ? -(q0 + q1) : q0 + q1;
               contrib = make_double2(op.kr * warp_sum1(q), 0.0);
             } else {
-              reg_op_any<R, 3>(v, l, op, c, q0, q1, z, z2);
               if (fold) z = make_double2(-z.x, -z.y);
               z = warp_sum(z);
               z2 = warp_sum(z2);
@@ -368,10 +381,29 @@ __global__ void __launch_bounds__(kRegThreads, 2) k_pass_reg(double2* __restrict
   }
 }
 
-template __global__ void k_pass_reg<kRegBits, 1>(double2*, double2*, const PassDesc, const SegDesc*, const RegOp*,
-                                                 const DevOp*, const double2*, double2*);
-template __global__ void k_pass_reg<kRegBits, 2>(double2*, double2*, const PassDesc, const SegDesc*, const RegOp*,
-                                                 const DevOp*, const double2*, double2*);
+#define SVGB_INST(R, NB)                                                                                   \
+  template __global__ void k_pass_reg<R, NB>(double2*, double2*, const PassDesc, const SegDesc*, const RegOp*, \
+                                             const DevOp*, const double2*, double2*);
+SVGB_INST(3, 1)
+SVGB_INST(3, 2)
+SVGB_INST(4, 1)
+SVGB_INST(4, 2)
+#undef SVGB_INST
+
+namespace {
+const void* reg_kernel(int nb, int R) {
+  if (R == 4) return nb == 1 ? reinterpret_cast<const void*>(k_pass_reg<4, 1>) : reinterpret_cast<const void*>(k_pass_reg<4, 2>);
+  return nb == 1 ? reinterpret_cast<const void*>(k_pass_reg<3, 1>) : reinterpret_cast<const void*>(k_pass_reg<3, 2>);
+}
+
+cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaFuncGetAttributes(&attr, fn);
+  if (e != cudaSuccess) return e;
+  const size_t room = max_smem > attr.sharedSizeBytes ? max_smem - attr.sharedSizeBytes : 0;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(room));
+}
+}  // namespace
 
 size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles) {
   return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(RegOp) * nops;
@@ -379,35 +411,35 @@ size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles) {
 
 int reg_max_threads() { return kRegThreads; }
 
-static cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
-  cudaFuncAttributes attr;
-  cudaError_t e = cudaFuncGetAttributes(&attr, fn);
-  if (e != cudaSuccess) return e;
-  const size_t room = max_smem > attr.sharedSizeBytes ? max_smem - attr.sharedSizeBytes : 0;
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(room));
-}
-
 cudaError_t prepare_reg_kernels(size_t max_smem) {
-  cudaError_t e = allow_dynamic_smem(reinterpret_cast<const void*>(k_pass_reg<kRegBits, 1>), max_smem);
-  if (e != cudaSuccess) return e;
-  return allow_dynamic_smem(reinterpret_cast<const void*>(k_pass_reg<kRegBits, 2>), max_smem);
+  for (int R = 3; R <= 4; ++R)
+    for (int nb = 1; nb <= 2; ++nb) {
+      const cudaError_t e = allow_dynamic_smem(reg_kernel(nb, R), max_smem);
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
 }
 
-int reg_occupancy(int nb, int threads, size_t smem) {
+int reg_occupancy(int nb, int R, int threads, size_t smem) {
   int blocks = 0;
-  const void* fn = nb == 1 ? reinterpret_cast<const void*>(k_pass_reg<kRegBits, 1>)
-                           : reinterpret_cast<const void*>(k_pass_reg<kRegBits, 2>);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, reg_kernel(nb, R), threads, smem);
   return blocks < 1 ? 1 : blocks;
 }
 
-void launch_pass_reg(int nb, const PassDesc& d, int grid, int threads, size_t smem, cudaStream_t s, double2* b0,
+void launch_pass_reg(int nb, int R, const PassDesc& d, int grid, int threads, size_t smem, cudaStream_t s, double2* b0,
                      double2* b1, const SegDesc* segs, const RegOp* rops, const DevOp* ops, const double2* coef,
                      double2* partials) {
-  if (nb == 1)
-    k_pass_reg<kRegBits, 1><<<grid, threads, smem, s>>>(b0, b1, d, segs, rops, ops, coef, partials);
-  else
-    k_pass_reg<kRegBits, 2><<<grid, threads, smem, s>>>(b0, b1, d, segs, rops, ops, coef, partials);
+  if (R == 4) {
+    if (nb == 1)
+      k_pass_reg<4, 1><<<grid, threads, smem, s>>>(b0, b1, d, segs, rops, ops, coef, partials);
+    else
+      k_pass_reg<4, 2><<<grid, threads, smem, s>>>(b0, b1, d, segs, rops, ops, coef, partials);
+  } else {
+    if (nb == 1)
+      k_pass_reg<3, 1><<<grid, threads, smem, s>>>(b0, b1, d, segs, rops, ops, coef, partials);
+    else
+      k_pass_reg<3, 2><<<grid, threads, smem, s>>>(b0, b1, d, segs, rops, ops, coef, partials);
+  }
 }
 
 }  // namespace svgb
