@@ -213,6 +213,7 @@ def run_ours(args, rank, world, local_rank):
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     rev_ms, rev_launches, launches, pass_bytes, last, tile_k = 0.0, 0, 0, 0, None, 0
+    phases = {"forward": 0.0, "observable": 0.0, "reverse": 0.0, "other": 0.0}
     with ClockSampler(local_rank) as clocks:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
@@ -221,10 +222,13 @@ def run_ours(args, rank, world, local_rank):
             last = step(basis, st)
             ev[i][1].record(stream)
             rev_ms += st["ms_reverse"]
+            for key in phases:
+                phases[key] += st[f"ms_{key}"] / args.steps
             rev_launches += st["rev_passes"]
             launches += st["launches"]
             pass_bytes = st["pass_bytes"]
             tile_k = st["tile_qubits"]
+            st_last = st
         torch.cuda.synchronize()
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     if dist:
@@ -289,7 +293,10 @@ def run_ours(args, rank, world, local_rank):
             "traffic": traffic, "kernel": "k_rev_pass", "bytes_per_launch": 4 * S,
             "avg_launch_ms": avg_launch_ms, "peak_source": peak_src,
         },
-        "effective_gate_level_gbs": B_alg / (total_ms / args.steps * 1e-3) / 1e9 / 1.0,
+        "phase_ms": {k: round(v, 4) for k, v in phases.items()},
+        "passes": {"forward": int(st_last["fwd_passes"]), "observable": int(st_last["obs_passes"]),
+                   "reverse": int(st_last["rev_passes"])},
+        "effective_gate_level_gbs": B_alg / (total_ms / args.steps * 1e-3) / 1e9,
         "pass_level_gbs": pass_bytes / (total_ms / args.steps * 1e-3) / 1e9,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
     }
