@@ -134,6 +134,8 @@ typedef struct {
   int64_t pass_bytes;        /* HBM state bytes the passes must move (read+write) */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  int32_t segments;          /* register-tile segments over all passes (0: shared-memory kernels) */
+  int32_t reg_bits;          /* amplitudes per thread per buffer = 2^reg_bits (register kernels) */
 } svg_stats;
 
 typedef struct svg_engine svg_engine;

@@ -73,7 +73,7 @@ class svg_stats(C.Structure):
         ("ms_reverse", C.c_double), ("ms_other", C.c_double), ("launches", C.c_int64),
         ("fwd_passes", C.c_int32), ("obs_passes", C.c_int32), ("rev_passes", C.c_int32),
         ("tile_qubits", C.c_int32), ("pass_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
-        ("d2h_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64), ("segments", C.c_int32), ("reg_bits", C.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -457,14 +457,15 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     for (size_t pi = 0; pi < gpasses.size(); ++pi) {
       const Pass& ps = gpasses[pi];
       const TileMap tm = tile_map(ps.qmask);
-      std::vector<uint32_t> flips(ps.items.size());
+      std::vector<uint32_t> flips(ps.items.size()), touch(ps.items.size());
       std::vector<char> dense(ps.items.size());
       for (size_t j = 0; j < ps.items.size(); ++j) {
         const svg_gate& g = p->gates[ps.items[j]];
         flips[j] = tm.local(shapes[ps.items[j]].flip);
+        touch[j] = tm.local(shapes[ps.items[j]].touch);
         dense[j] = !reg_capable(g, flips[j]);
       }
-      psegs[pi] = plan_segments(flips, dense, L.k, RB);
+      psegs[pi] = plan_segments(flips, touch, dense, L.k, RB);
     }
   }
   auto reg_launch = [&](const Pass& ps, int nb) {
@@ -833,6 +834,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       stats->obs_passes = static_cast<int32_t>(L.obs.size());
       stats->rev_passes = static_cast<int32_t>(L.rev.size());
       stats->tile_qubits = L.k;
+      stats->segments = L.reg ? static_cast<int32_t>(L.segs.size()) : 0;
+      stats->reg_bits = L.reg ? L.R : 0;
       stats->pass_bytes = L.pass_bytes;
       stats->h2d_bytes = h2d;
       stats->d2h_bytes = d2h;

@@ -94,31 +94,108 @@ std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, cons
   return passes;
 }
 
-std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<char>& dense, int k,
-                                   int regbits) {
+std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
+                                   const std::vector<char>& dense, int k, int regbits) {
   const uint32_t lanes = 31u;
   const uint32_t nonlane = ((k >= 32) ? ~0u : ((1u << k) - 1)) & ~lanes;
-  std::vector<Segment> segs;
-  Segment cur;
-  auto flush = [&]() {
-    if (!cur.items.empty()) segs.push_back(cur);
-    cur = Segment();
-  };
   const int m = static_cast<int>(flip_pos.size());
-  for (int i = 0; i < m; ++i) {
-    if (dense[i]) {
-      if (cur.reg) flush();
-      cur.reg = false;
-      cur.items.push_back(i);
+  // Dependencies inside the pass: i < j conflict when they share a tile
+  // position that either of them flips (everything else commutes; positions
+  // outside the tile are diagonal for every gate of the pass).
+  std::vector<std::vector<int>> succ(m);
+  std::vector<int> npred(m, 0);
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) {
+      const uint32_t shared = touch_pos[i] & touch_pos[j];
+      if (shared & (flip_pos[i] | flip_pos[j])) {
+        succ[i].push_back(j);
+        ++npred[j];
+      }
+    }
+  std::vector<char> done(m, 0);
+  int remaining = m;
+  // Gates runnable (transitively) with register set `regs`; `commit` applies them.
+  auto closure = [&](uint32_t regs, std::vector<int>* order) {
+    std::vector<int> pred = npred;
+    std::vector<char> taken(done);
+    int count = 0;
+    bool progress = true;
+    while (progress) {
+      progress = false;
+      for (int i = 0; i < m; ++i) {
+        if (taken[i] || pred[i] != 0 || dense[i] || (flip_pos[i] & nonlane & ~regs)) continue;
+        taken[i] = 1;
+        ++count;
+        progress = true;
+        if (order) order->push_back(i);
+        for (int j : succ[i]) --pred[j];
+      }
+    }
+    return count;
+  };
+  auto retire = [&](const std::vector<int>& order) {
+    for (int i : order) {
+      done[i] = 1;
+      --remaining;
+      for (int j : succ[i]) --npred[j];
+    }
+  };
+  std::vector<Segment> segs;
+  while (remaining > 0) {
+    // dense gates that are ready run as a shared-memory segment
+    Segment sm;
+    sm.reg = false;
+    for (bool progress = true; progress;) {
+      progress = false;
+      for (int i = 0; i < m; ++i)
+        if (!done[i] && dense[i] && npred[i] == 0) {
+          sm.items.push_back(i);
+          retire({i});
+          progress = true;
+          break;
+        }
+    }
+    if (!sm.items.empty()) {
+      segs.push_back(sm);
       continue;
     }
-    if (!cur.reg) flush();
-    const uint32_t f = flip_pos[i] & nonlane;
-    if (popc(cur.regmask | f) > regbits) flush();
-    cur.regmask |= f;
-    cur.items.push_back(i);
+    // choose the register set greedily by how many gates it unlocks
+    uint32_t regs = 0;
+    int best_count = closure(0, nullptr);
+    while (popc(regs) < regbits) {
+      uint32_t cand_mask = 0;
+      for (int i = 0; i < m; ++i)
+        if (!done[i] && !dense[i]) cand_mask |= flip_pos[i] & nonlane & ~regs;
+      if (!cand_mask) break;
+      int best = -1, best_pos = -1;
+      for (uint32_t v = cand_mask; v; v &= v - 1) {
+        const int p = __builtin_ctz(v);
+        const int c = closure(regs | (1u << p), nullptr);
+        if (c > best) {
+          best = c;
+          best_pos = p;
+        }
+      }
+      if (best <= best_count && popc(regs) > 0) {
+        // no single position helps: take the flip set of the earliest pending gate
+        for (int i = 0; i < m; ++i)
+          if (!done[i] && !dense[i] && npred[i] == 0 && popc(regs | (flip_pos[i] & nonlane)) <= regbits &&
+              (flip_pos[i] & nonlane & ~regs)) {
+            regs |= flip_pos[i] & nonlane;
+            break;
+          }
+        break;
+      }
+      regs |= 1u << best_pos;
+      best_count = best;
+    }
+    Segment sg;
+    sg.regmask = regs;
+    closure(regs, &sg.items);
+    if (sg.items.empty()) throw std::runtime_error("segment planner made no progress");
+    retire(sg.items);
+    segs.push_back(sg);
   }
-  flush();
   // Fill each register set to exactly `regbits` positions, preferring the
   // positions the following segments flip (fewer distinct layouts overall).
   for (size_t s = 0; s < segs.size(); ++s) {

@@ -63,8 +63,10 @@ struct Segment {
   std::vector<int> items;   // indices into the pass's item list
   uint32_t regmask = 0;     // tile positions held in registers (reg segments)
 };
-std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<char>& dense, int k,
-                                   int regbits);
+// Gates may be reordered inside a pass (dependency-aware list scheduling):
+// each segment takes the register set that unlocks the most pending gates.
+std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
+                                   const std::vector<char>& dense, int k, int regbits);
 
 // Tile size choice for n qubits on `sms` SMs (auto when requested == 0).
 int choose_tile_qubits(int n, int requested, int sms);
