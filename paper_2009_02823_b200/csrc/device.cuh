@@ -55,7 +55,7 @@ struct PassDesc {
   int32_t untiled;       // observable pass over full-width masks (no tile)
   int32_t seg_begin, seg_end;  // register-tile passes: segment range
   int32_t smem_tiles;    // register-tile passes: 1 if the pass stages tiles in shared memory
-  int32_t pad0;
+  int32_t thread_acc;    // register-tile reverse passes: per-thread inner-product accumulators
   uint8_t q[kMaxQubits]; // tile qubits ascending
 };
 

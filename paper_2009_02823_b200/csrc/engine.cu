@@ -390,9 +390,18 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
       op.flags |= RF_IP3;
     }
   }
-  // flat code-path id, see run_variant in kernels_reg.cu
-  const uint32_t nshape = 2 + R;
-  const uint32_t shape_id = op.shape == RS_DIAG ? 0 : op.shape == RS_LANE ? 1 : 2 + __builtin_ctz(op.xr);
+  // flat code-path id, see Pat<R> and run_variant in kernels_reg.cu
+  const uint32_t P_DIAG = 0, P_DIAGZ = 1, P_LANE = 1 + R, P_REG = 2 + R, P_REGY = 2 + 2 * R, P_GDIAG = 2 + 3 * R,
+                 P_GLANE = 3 + 3 * R, P_GREG = 4 + 3 * R, NP = 4 + 4 * R;
+  uint32_t pattern;
+  if (op.shape == RS_DIAG)
+    pattern = zr == 0 ? P_DIAG : (__builtin_popcount(zr) == 1 ? P_DIAGZ + __builtin_ctz(zr) : P_GDIAG);
+  else if (op.shape == RS_LANE)
+    pattern = zr == 0 ? P_LANE : P_GLANE;
+  else {
+    const uint32_t b = __builtin_ctz(op.xr);
+    pattern = zr == 0 ? P_REG + b : (zr == op.xr ? P_REGY + b : P_GREG + b);
+  }
   uint32_t mode = bi ? 1 : 0;
   if (kind == ROP_REV) {
     if (op.flags & RF_IP3)
@@ -402,7 +411,7 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
     else
       mode = 2 + (bi ? 1 : 0);
   }
-  op.variant = shape_id + nshape * ((op.smask != 0) + 2 * ((cloc != 0) + 2 * mode));
+  op.variant = pattern + NP * ((cloc != 0) + 2 * mode);
   L.rops.push_back(op);
 }
 
@@ -652,7 +661,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         l.grid = clamp_grid(occupancy(2, l.smem));
         break;
       case L_REG:
-        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles);
+        // per-thread inner-product accumulators when they fit a modest budget
+        l.d.thread_acc = l.nb == 2 && size_t(l.d.nslots) * l.threads * sizeof(double) <= (48u << 10);
+        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles,
+                          l.d.thread_acc != 0);
         l.grid = clamp_grid(reg_occupancy(l.nb, L.R, l.threads, l.smem));
         break;
       case L_OBS:

@@ -106,110 +106,138 @@ __device__ __forceinline__ void from_smem(double2 (&v)[1 << R], const double2* s
 
 // Per-op, per-thread constants.
 struct OpCtx {
-  double a, bb;    // BI: new = a v + i bb ps ; else new = a v + bb ps
-  double2 bc;      // IPK 3 (generic): b' as a complex number
-  uint32_t slw;    // lane/warp/base part of the partner sign (0/1)
-  uint32_t smask, cmask;
+  double a, bb;    // new = a v + bb * (i^BI) * p   (bb carries the uniform part of the partner sign)
+  double2 bc;      // generic complex b' (reverse mode 6)
+  uint32_t smask;  // register part of the partner sign (runtime patterns only)
+  uint32_t cmask;  // register part of the control test
   bool clw_ok;     // lane/warp part of the control test
 };
 
-// One amplitude: v <- a v + b' ps   (ps already carries the partner sign)
+// Register-op patterns: flip shape and how the partner sign depends on the
+// register slot j.  Compile-time sign patterns cost nothing (negated FMA
+// operands); only the rare multi-bit Z patterns read the runtime smask.
+//   P_DIAG            diagonal, sign uniform
+//   P_DIAGZ + b       diagonal, sign_j = bit_b(j)               (RZ-type on register bit b)
+//   P_LANE            lane flip, sign uniform
+//   P_REG + b         flip register bit b, sign uniform         (RX-type)
+//   P_REGY + b        flip register bit b, sign_j = !bit_b(j)   (RY-type: Z on the flipped bit)
+//   P_GDIAG / P_GLANE / P_GREG + b   runtime smask
+template <int R>
+struct Pat {
+  static constexpr int DIAG = 0, DIAGZ = 1, LANE = 1 + R, REG = 2 + R, REGY = 2 + 2 * R, GDIAG = 2 + 3 * R,
+                       GLANE = 3 + 3 * R, GREG = 4 + 3 * R, N = 4 + 4 * R;
+};
+
+// v <- a v + (-1)^neg bb (i^BI p)      (in-place friendly: the DFMA overwrites v)
 template <int BI>
-__device__ __forceinline__ double2 upd(const OpCtx& c, double2 v, double2 ps) {
-  if (BI == 1) return make_double2(fma(-c.bb, ps.y, c.a * v.x), fma(c.bb, ps.x, c.a * v.y));
-  if (BI == 0) return make_double2(fma(c.bb, ps.x, c.a * v.x), fma(c.bb, ps.y, c.a * v.y));
-  return make_double2(fma(c.bc.x, ps.x, fma(-c.bc.y, ps.y, c.a * v.x)),
-                      fma(c.bc.x, ps.y, fma(c.bc.y, ps.x, c.a * v.y)));  // generic complex b'
+__device__ __forceinline__ double2 upd(const OpCtx& c, double2 v, double2 p, bool neg) {
+  double tx, ty;
+  if (BI == 1) {
+    tx = -c.bb * p.y;
+    ty = c.bb * p.x;
+  } else if (BI == 0) {
+    tx = c.bb * p.x;
+    ty = c.bb * p.y;
+  } else {
+    tx = fma(c.bc.x, p.x, -c.bc.y * p.y);
+    ty = fma(c.bc.x, p.y, c.bc.y * p.x);
+  }
+  if (neg) {
+    tx = -tx;
+    ty = -ty;
+  }
+  return make_double2(fma(c.a, v.x, tx), fma(c.a, v.y, ty));
 }
 
-// Inner-product terms for one amplitude with signed partner ps.
-// IPK 1: q += Re(conj(lam) sel(ps)) with sel = -i (BI: Im part) or 1 ; IPK 3: full z, z2.
+// Inner-product terms for one amplitude: partner p with sign (-1)^neg.
+// IPK 1: q += Re(conj(lam) sel(s p)), sel = -i (BI) or 1 ; IPK 3: z += conj(lam) s p, z2 += conj(lam) v.
 template <int IPK, int BI>
-__device__ __forceinline__ void ip_term(double lamx, double lamy, double2 ps, double2 v, double& q, double2& z,
+__device__ __forceinline__ void ip_term(double2 lam, double2 p, double2 v, bool neg, double& q, double2& z,
                                         double2& z2) {
+  const double lx = neg ? -lam.x : lam.x, ly = neg ? -lam.y : lam.y;  // sign folded into lambda (free negation)
   if (IPK == 1) {
     if (BI == 1)
-      q = fma(lamx, ps.y, fma(-lamy, ps.x, q));
+      q = fma(lx, p.y, fma(-ly, p.x, q));
     else
-      q = fma(lamx, ps.x, fma(lamy, ps.y, q));
+      q = fma(lx, p.x, fma(ly, p.y, q));
   } else if (IPK == 3) {
-    z.x = fma(lamx, ps.x, fma(lamy, ps.y, z.x));
-    z.y = fma(lamx, ps.y, fma(-lamy, ps.x, z.y));
-    z2.x = fma(lamx, v.x, fma(lamy, v.y, z2.x));
-    z2.y = fma(lamx, v.y, fma(-lamy, v.x, z2.y));
+    z.x = fma(lx, p.x, fma(ly, p.y, z.x));
+    z.y = fma(lx, p.y, fma(-ly, p.x, z.y));
+    z2.x = fma(lam.x, v.x, fma(lam.y, v.y, z2.x));
+    z2.y = fma(lam.x, v.y, fma(-lam.y, v.x, z2.y));
   }
 }
 
-// Apply one op to register tile v; SHAPE: RS_DIAG / RS_LANE / RS_REG (flip bit XB).
-// For IPK != 0, `l` is lambda (read only) and the inner product uses the
-// pre-update v (phi_{i+1}).  BI: 0/1 = real/imaginary b' (and generator), 2 = generic.
-// SIGNED: the partner sign varies with the register slot (smask != 0);
-// otherwise it is uniform per op and was folded into the coefficients.
-// DUAL: the same operator is also applied to the lambda tile `l` (reverse
-// pass: for a unitary Pauli-form gate the rewind R = U^-1 equals U^dag, so
-// phi and lambda share one op, its partner signs and its controls).
-template <int R, int SHAPE, int XB, int IPK, int BI, bool CTRL, bool SIGNED, bool DUAL>
+// Sign of the partner of register slot j for pattern P (compile-time unless runtime pattern).
+template <int R, int P>
+__device__ __forceinline__ bool psign(const OpCtx& c, int j) {
+  using PT = Pat<R>;
+  if constexpr (P >= PT::DIAGZ && P < PT::LANE) return (j >> (P - PT::DIAGZ)) & 1;
+  else if constexpr (P >= PT::REGY && P < PT::GDIAG) return !((j >> (P - PT::REGY)) & 1);
+  else if constexpr (P >= PT::GDIAG) return (c.smask >> j) & 1u;
+  else return false;
+}
+
+// One op on the register tile v (and, DUAL, the same op on lambda l).  For
+// IPK != 0 the inner product uses lambda and phi before the update (phi_{i+1}).
+template <int R, int P, int IPK, int BI, bool CTRL, bool DUAL>
 __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
                                        double& q0, double& q1, double2& z, double2& z2) {
+  using PT = Pat<R>;
   constexpr int NR = 1 << R;
-  constexpr int XR = (SHAPE == RS_REG) ? (1 << XB) : 0;
+  constexpr bool LANEF = (P == PT::LANE || P == PT::GLANE);
+  constexpr int XB = (P >= PT::REG && P < PT::GDIAG) ? (P - PT::REG) % R : (P >= PT::GREG ? P - PT::GREG : -1);
+  constexpr int XR = XB >= 0 ? (1 << XB) : 0;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     if (XR != 0 && (j & XR)) continue;  // register pairs handled at the low member
     const int jp = j ^ XR;
-    const uint32_t sj = SIGNED ? (((c.smask >> j) & 1u) ^ c.slw) : 0u;
-    const uint32_t sp = SIGNED ? (((c.smask >> jp) & 1u) ^ c.slw) : 0u;
+    const bool sj = psign<R, P>(c, j);
     const bool okj = !CTRL || (c.clw_ok && ((c.cmask >> j) & 1u));
     double2 pj = v[jp];  // partner of slot j (slot jp of the partner lane)
-    if (SHAPE == RS_LANE) pj = shfl2(pj, xl);
-    const double2 psj = SIGNED ? sflip(pj, sj) : pj;
-    double2 lpj = make_double2(0.0, 0.0);
-    if (DUAL) {
-      lpj = l[jp];
-      if (SHAPE == RS_LANE) lpj = shfl2(lpj, xl);
-      if (SIGNED) lpj = sflip(lpj, sj);
+    double2 lpj = DUAL ? l[jp] : pj;
+    if (LANEF) {
+      pj = shfl2(pj, xl);
+      if (DUAL) lpj = shfl2(lpj, xl);
     }
-    if (IPK != 0 && okj) ip_term<IPK, BI>(l[j].x, l[j].y, psj, v[j], (j & 1) ? q1 : q0, z, z2);
-    const double2 nj = upd<BI>(c, v[j], psj);
-    const double2 lnj = DUAL ? upd<BI>(c, l[j], lpj) : lpj;
-    if (XR != 0) {
-      const double2 psp = SIGNED ? sflip(v[j], sp) : v[j];
-      if (IPK != 0 && okj) ip_term<IPK, BI>(l[jp].x, l[jp].y, psp, v[jp], q1, z, z2);
-      const double2 np = upd<BI>(c, v[jp], psp);
-      if (!CTRL || okj) v[jp] = np;
-      if (DUAL) {
-        const double2 lnp = upd<BI>(c, l[jp], SIGNED ? sflip(l[j], sp) : l[j]);
-        if (!CTRL || okj) l[jp] = lnp;
+    if (IPK != 0 && okj) ip_term<IPK, BI>(l[j], pj, v[j], sj, (j & 1) ? q1 : q0, z, z2);
+    if (XR == 0) {
+      if (!CTRL || okj) {
+        v[j] = upd<BI>(c, v[j], pj, sj);
+        if (DUAL) l[j] = upd<BI>(c, l[j], lpj, sj);
       }
-    }
-    if (!CTRL || okj) {
-      v[j] = nj;
-      if (DUAL) l[j] = lnj;
+    } else {
+      const bool sp = psign<R, P>(c, jp);
+      if (IPK != 0 && okj) ip_term<IPK, BI>(l[jp], v[j], v[jp], sp, q1, z, z2);
+      if (!CTRL || okj) {
+        const double2 vj = v[j], lj = l[j];
+        v[j] = upd<BI>(c, vj, pj, sj);
+        v[jp] = upd<BI>(c, v[jp], vj, sp);
+        if (DUAL) {
+          l[j] = upd<BI>(c, lj, lpj, sj);
+          l[jp] = upd<BI>(c, l[jp], lj, sp);
+        }
+      }
     }
   }
 }
 
 // Flat variant id (computed on the host, see engine.cu emit_rop):
-//   id = shape + NSHAPE * (signed + 2 * (ctrl + 2 * mode)),  NSHAPE = 2 + R
-//   shape: 0 diagonal, 1 lane flip, 2 + b register-bit-b flip
-//   mode:  0/1 forward (BI 0/1); 2/3 reverse IPK 0 (BI 0/1); 4/5 reverse IPK 1 (BI 0/1);
-//          6 reverse IPK 3 (generic complex coefficients)
+//   id = pattern + Pat<R>::N * (ctrl + 2 * mode)
+//   mode: 0/1 forward (BI 0/1); 2/3 reverse IPK 0 (BI 0/1); 4/5 reverse IPK 1 (BI 0/1);
+//         6 reverse IPK 3 (generic complex coefficients)
 template <int R, int NB, int V>
 __device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
                                             double& q0, double& q1, double2& z, double2& z2) {
-  constexpr int NSHAPE = 2 + R;
-  constexpr int NV = NSHAPE * 4 * 7;
-  if constexpr (V < NV) {
-    constexpr int shape = V % NSHAPE;
-    constexpr bool SIGNED = (V / NSHAPE) % 2;
-    constexpr bool CTRL = (V / NSHAPE / 2) % 2;
-    constexpr int mode = V / NSHAPE / 4;
-    constexpr int SH = shape == 0 ? RS_DIAG : (shape == 1 ? RS_LANE : RS_REG);
-    constexpr int XB = shape >= 2 ? shape - 2 : 0;
+  constexpr int NP = Pat<R>::N;
+  if constexpr (V < NP * 2 * 7) {
+    constexpr int P = V % NP;
+    constexpr bool CTRL = (V / NP) % 2;
+    constexpr int mode = V / NP / 2;
     constexpr bool DUAL = mode >= 2;
     constexpr int IPK = mode >= 6 ? 3 : (mode >= 4 ? 1 : 0);
     constexpr int BI = mode == 6 ? 2 : (mode & 1);
-    if constexpr (NB == 2 || !DUAL) reg_op<R, SH, XB, IPK, BI, CTRL, SIGNED, DUAL>(v, l, c, xl, q0, q1, z, z2);
+    if constexpr (NB == 2 || !DUAL) reg_op<R, P, IPK, BI, CTRL, DUAL>(v, l, c, xl, q0, q1, z, z2);
   }
 }
 
@@ -224,10 +252,13 @@ __device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1
 template <int R, int NB>
 __device__ __forceinline__ void dispatch(uint32_t id, double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c,
                                          uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
+  static_assert(Pat<R>::N * 2 * 7 <= 320, "extend the dispatch table");
   switch (id) {
     SVGB_V64(0)
     SVGB_V64(64)
     SVGB_V64(128)
+    SVGB_V64(192)
+    SVGB_V64(256)
     default:
       break;
   }
@@ -262,9 +293,12 @@ __global__ void __launch_bounds__(kRegThreads, R == 3 ? 2 : 1) k_pass_reg(double
   double2* wacc = reinterpret_cast<double2*>(smem_raw);  // [nwarps][nslots]
   RegOp* sops = reinterpret_cast<RegOp*>(wacc + nwarps * d.nslots);  // this pass's register ops
   const int nops = d.op_end - d.op_begin;
-  double2* st0 = reinterpret_cast<double2*>(sops + nops);  // shared tiles (multi-segment passes)
-  double2* st1 = st0 + (1u << d.k);
+  double* tacc = d.thread_acc ? reinterpret_cast<double*>(sops + nops) : nullptr;  // [nslots][nthr]
+  double2* st0 = reinterpret_cast<double2*>(sops + nops) + (d.thread_acc ? (d.nslots * nthr + 1) / 2 : 0);
+  double2* st1 = st0 + (1u << d.k);  // shared tiles (multi-segment passes)
   for (int i = threadIdx.x; i < nwarps * d.nslots; i += nthr) wacc[i] = make_double2(0.0, 0.0);
+  if (tacc)
+    for (int i = threadIdx.x; i < d.nslots * nthr; i += nthr) tacc[i] = 0.0;
   {
     const uint4* src = reinterpret_cast<const uint4*>(rops + d.op_begin);
     uint4* dst = reinterpret_cast<uint4*>(sops);
@@ -303,38 +337,35 @@ __global__ void __launch_bounds__(kRegThreads, R == 3 ? 2 : 1) k_pass_reg(double
         for (int o = sg.op_begin - d.op_begin; o < sg.op_end - d.op_begin; ++o) {
           const RegOp& op = sops[o];
           if ((base & op.co) != op.co) continue;
+          const uint32_t slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(base & op.zo)) & 1u;
           OpCtx c;
           c.a = op.a;
-          c.bb = op.bb;
-          c.bc = (op.flags & RF_BI) ? make_double2(0.0, op.bb) : make_double2(op.bb, 0.0);
-          c.slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(base & op.zo)) & 1u;
+          c.bb = slw ? -op.bb : op.bb;  // uniform part of the partner sign
+          c.bc = (op.flags & RF_BI) ? make_double2(0.0, c.bb) : make_double2(c.bb, 0.0);
           c.smask = op.smask;
           c.cmask = op.cmask;
           c.clw_ok = (tbase & op.clw) == op.clw;
-          // uniform partner sign: fold into the coefficient (and into the IP result below)
-          const bool fold = op.smask == 0 && c.slw;
-          if (fold) {
-            c.bb = -c.bb;
-            c.bc = make_double2(-c.bc.x, -c.bc.y);
-          }
           double q0 = 0.0, q1 = 0.0;
           double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
           dispatch<R, NB>(op.variant, v, l, c, op.xl, q0, q1, z, z2);
           if constexpr (NB == 2) {
-            if (!(op.flags & (RF_IP1 | RF_IP3))) continue;
-            double2 contrib;
-            if (op.flags & RF_IP1) {
-              const double q = fold ? -(q0 + q1) : q0 + q1;
-              contrib = make_double2(op.kr * warp_sum1(q), 0.0);
-            } else {
-              if (fold) z = make_double2(-z.x, -z.y);
+            if (op.flags & RF_IP1) {  // per-thread accumulator: no per-op warp reduction
+              const double q = op.kr * (slw ? -(q0 + q1) : q0 + q1);
+              if (tacc) {
+                tacc[op.slot * nthr + threadIdx.x] += q;
+              } else {
+                const double w = warp_sum1(q);
+                if (lane == 0) wacc[warp * d.nslots + op.slot].x += w;
+              }
+            } else if (op.flags & RF_IP3) {
+              if (slw) z = make_double2(-z.x, -z.y);
               z = warp_sum(z);
               z2 = warp_sum(z2);
-              contrib = cfma(op.kb, z, cmul(op.ka, z2));
-            }
-            if (lane == 0) {
-              double2& acc = wacc[warp * d.nslots + op.slot];
-              acc = make_double2(acc.x + contrib.x, acc.y + contrib.y);
+              const double2 contrib = cfma(op.kb, z, cmul(op.ka, z2));
+              if (lane == 0) {
+                double2& acc = wacc[warp * d.nslots + op.slot];
+                acc = make_double2(acc.x + contrib.x, acc.y + contrib.y);
+              }
             }
           }
         }
@@ -377,6 +408,8 @@ __global__ void __launch_bounds__(kRegThreads, R == 3 ? 2 : 1) k_pass_reg(double
       const double2 val = wacc[w * d.nslots + s];
       acc = make_double2(acc.x + val.x, acc.y + val.y);
     }
+    if (tacc)
+      for (int t = 0; t < nthr; ++t) acc.x += tacc[s * nthr + t];
     partials[d.part_off + static_cast<int64_t>(s) * gridDim.x + blockIdx.x] = acc;
   }
 }
@@ -405,8 +438,9 @@ cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
 }
 }  // namespace
 
-size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles) {
-  return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(RegOp) * nops;
+size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles, bool thread_acc) {
+  const size_t tacc = thread_acc ? sizeof(double2) * ((size_t(nslots) * nwarps * 32 + 1) / 2) : 0;
+  return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(RegOp) * nops + tacc;
 }
 
 int reg_max_threads() { return kRegThreads; }
