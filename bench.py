@@ -52,7 +52,8 @@ def _args():
     ap.add_argument("--qubits", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tile-qubits", type=int, default=0)
-    ap.add_argument("--reg-bits", type=int, default=0, help="register-tile amplitudes per thread = 2^bits (3/4)")
+    ap.add_argument("--reg-bits", type=int, default=0, help="reverse register tile: 2^bits amplitudes/thread (3/4)")
+    ap.add_argument("--reg-bits-fwd", type=int, default=0, help="forward register tile: 2^bits amplitudes/thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -196,6 +197,8 @@ def run_ours(args, rank, world, local_rank):
     eng.set_option("tile_qubits", args.tile_qubits)
     if args.reg_bits:
         eng.set_option("reg_bits", args.reg_bits)
+    if args.reg_bits_fwd:
+        eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

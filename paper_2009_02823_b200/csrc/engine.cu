@@ -114,6 +114,7 @@ struct Launch {
   int kind = L_SMEM_FWD;
   int nb = 1;       // L_REG: buffers in the pass (1 forward, 2 reverse)
   int threads = kThreads;
+  int R = 3;           // L_REG: register bits
   bool tiles = false;  // L_REG: stages the tile through shared memory
 };
 
@@ -149,7 +150,7 @@ struct svg_engine {
   size_t max_smem = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 3;
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4;
   DeviceBuf psi, lam, partials, blob, results;
   HostBuf hblob, hres;
   cudaEvent_t ev[6] = {};
@@ -402,14 +403,18 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
     const uint32_t b = __builtin_ctz(op.xr);
     pattern = zr == 0 ? P_REG + b : (zr == op.xr ? P_REGY + b : P_GREG + b);
   }
-  uint32_t mode = bi ? 1 : 0;
+  // pure Pauli (X/Y/Z, CX, ...): a signed permutation without arithmetic
+  const bool perm = op.a == 0.0 && std::fabs(op.bb) == 1.0 && !kpost;
+  uint32_t mode = perm ? 2 + (bi ? 1 : 0) : (bi ? 1 : 0);
   if (kind == ROP_REV) {
     if (op.flags & RF_IP3)
       mode = 6;
     else if (op.flags & RF_IP1)
       mode = 4 + (bi ? 1 : 0);
+    else if (perm)
+      mode = 7 + (bi ? 1 : 0);
     else
-      mode = 2 + (bi ? 1 : 0);
+      throw std::logic_error("parameter-free non-permutation Pauli op reached the register path");
   }
   op.variant = pattern + NP * ((cloc != 0) + 2 * mode);
   L.rops.push_back(op);
@@ -426,6 +431,8 @@ bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
   for (const svg_c128* c : {g.fwd, g.rewind, g.adjoint}) {
     const double2 b = cm(d2(c[1]), ph);
     if (c[0].im != 0.0 || (b.x != 0.0 && b.y != 0.0)) return false;
+    // parameter-free ops must be signed permutations (the reverse kernel has no plain-rewind mode)
+    if (g.nderiv == 0 && (c[0].re != 0.0 || std::fabs(b.x + b.y) != 1.0)) return false;
   }
   const uint32_t hi = flip_tile & ~31u;
   if (hi == 0) return true;
@@ -439,10 +446,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   L.n = n;
   L.k = choose_tile_qubits(n, static_cast<int>(e->opt_tile), e->sms);
   L.b = (n <= L.k) ? n : std::min(5, L.k - 2);
-  const int RB = static_cast<int>(e->opt_reg_bits);
+  const int RB = static_cast<int>(e->opt_reg_bits);      // reverse passes
+  const int RF = static_cast<int>(e->opt_reg_bits_fwd);  // forward passes
   L.R = RB;
-  const int wbits = L.k - 5 - RB;
-  L.reg = e->opt_kernel != 1 && L.b >= 5 && wbits >= 0 && (32 << wbits) <= reg_max_threads();
+  auto fits = [&](int R) { return L.k - 5 - R >= 0 && (32 << (L.k - 5 - R)) <= reg_max_threads(R); };
+  L.reg = e->opt_kernel != 1 && L.b >= 5 && fits(RB) && fits(RF);
   if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 5 + reg_bits .. 13 tile qubits");
   PlanParams pp;
   pp.n = n;
@@ -461,7 +469,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   for (int d = 0; d < p->num_derivs; ++d) gens[d] = make_gen(p->gates[p->derivs[d].gate], p->derivs[d]);
 
   // segments per pass (register path)
-  std::vector<std::vector<Segment>> psegs(gpasses.size());
+  std::vector<std::vector<Segment>> psegs(gpasses.size()), psegs_f(gpasses.size());
   if (L.reg) {
     for (size_t pi = 0; pi < gpasses.size(); ++pi) {
       const Pass& ps = gpasses[pi];
@@ -475,6 +483,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         dense[j] = !reg_capable(g, flips[j]);
       }
       psegs[pi] = plan_segments(flips, touch, dense, L.k, RB);
+      psegs_f[pi] = RF == RB ? psegs[pi] : plan_segments(flips, touch, dense, L.k, RF);
     }
   }
   auto reg_launch = [&](const Pass& ps, int nb) {
@@ -482,13 +491,14 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     l.d = make_desc(n, L.k, ps.qmask);
     l.kind = L_REG;
     l.nb = nb;
-    l.threads = 32 << wbits;
+    l.R = nb == 1 ? RF : RB;
+    l.threads = 32 << (L.k - 5 - l.R);
     l.d.seg_begin = static_cast<int>(L.segs.size());
     l.d.op_begin = static_cast<int>(L.rops.size());  // this pass's register ops (staged in smem)
     return l;
   };
   // default register layout for shared-memory segments: lowest non-lane positions
-  const uint32_t default_regs = ((1u << (5 + RB)) - 1u) & ~31u;
+  auto default_regs = [](int R) { return ((1u << (5 + R)) - 1u) & ~31u; };
 
   // forward passes
   for (size_t pi = 0; pi < gpasses.size(); ++pi) {
@@ -505,9 +515,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     } else {
       Launch l = reg_launch(ps, 1);
       uint32_t prev = ~0u;
-      for (const Segment& sg : psegs[pi]) {
+      for (const Segment& sg : psegs_f[pi]) {
         SegLocal sl;
-        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, RB, &sl);
+        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF), L.k, RF, &sl);
         sd.same_map = sg.reg && sg.regmask == prev;
         prev = sg.reg ? sg.regmask : ~0u;
         if (sg.reg) {
@@ -527,7 +537,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
       l.d.seg_end = static_cast<int>(L.segs.size());
       l.d.op_end = static_cast<int>(L.rops.size());
-      if (psegs[pi].size() > 1) l.tiles = true;
+      if (psegs_f[pi].size() > 1) l.tiles = true;
       L.fwd.push_back(l);
     }
     L.pass_bytes += 2 * S;
@@ -607,7 +617,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
           const Segment& sg = *st;
           SegLocal sl;
-          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs, L.k, RB, &sl);
+          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RB), L.k, RB, &sl);
           sd.same_map = sg.reg && sg.regmask == prev;
           prev = sg.reg ? sg.regmask : ~0u;
           if (sg.reg) {
@@ -665,7 +675,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         l.d.thread_acc = l.nb == 2 && size_t(l.d.nslots) * l.threads * sizeof(double) <= (48u << 10);
         l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles,
                           l.d.thread_acc != 0);
-        l.grid = clamp_grid(reg_occupancy(l.nb, L.R, l.threads, l.smem));
+        l.grid = clamp_grid(reg_occupancy(l.nb, l.R, l.threads, l.smem));
         break;
       case L_OBS:
         l.smem = obs_smem(L.k, l.d.b);
@@ -788,7 +798,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     CK(cudaEventRecord(e->ev[1], s));
     for (const Launch& l : L.fwd) {
       if (l.kind == L_REG)
-        launch_pass_reg(1, L.R, l.d, l.grid, l.threads, l.smem, s, psi, nullptr, dsegs, drops, dops, dcoef, part);
+        launch_pass_reg(1, l.R, l.d, l.grid, l.threads, l.smem, s, psi, nullptr, dsegs, drops, dops, dcoef, part);
       else
         launch_fwd(l.d, l.grid, l.smem, s, psi, dops, dcoef);
     }
@@ -802,7 +812,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     CK(cudaEventRecord(e->ev[3], s));
     for (const Launch& l : L.rev) {
       if (l.kind == L_REG)
-        launch_pass_reg(2, L.R, l.d, l.grid, l.threads, l.smem, s, psi, lam, dsegs, drops, dops, dcoef, part);
+        launch_pass_reg(2, l.R, l.d, l.grid, l.threads, l.smem, s, psi, lam, dsegs, drops, dops, dcoef, part);
       else
         launch_rev(l.d, l.grid, l.smem, s, psi, lam, dops, dcoef, part);
     }
@@ -949,9 +959,10 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     e->opt_tile = value;
   } else if (k == "profile") {
     e->opt_profile = value;
-  } else if (k == "reg_bits") {
-    if (value != 3 && value != 4) return fail(SVG_EINVAL, "reg_bits must be 3 or 4");
-    e->opt_reg_bits = value;
+  } else if (k == "reg_bits" || k == "reg_bits_fwd") {
+    if (value == 0) value = 4;
+    if (value != 3 && value != 4) return fail(SVG_EINVAL, k + " must be 3 or 4");
+    (k == "reg_bits" ? e->opt_reg_bits : e->opt_reg_bits_fwd) = value;
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;

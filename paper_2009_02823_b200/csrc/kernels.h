@@ -30,7 +30,7 @@ void launch_set_basis(double2* psi, uint64_t idx, cudaStream_t s);
 size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles, bool thread_acc);
 cudaError_t prepare_reg_kernels(size_t max_smem);
 int reg_occupancy(int nb, int R, int threads, size_t smem);
-int reg_max_threads();
+int reg_max_threads(int R);
 void launch_pass_reg(int nb, int R, const PassDesc& d, int grid, int threads, size_t smem, cudaStream_t s, double2* b0,
                      double2* b1, const SegDesc* segs, const RegOp* rops, const DevOp* ops, const double2* coef,
                      double2* partials);

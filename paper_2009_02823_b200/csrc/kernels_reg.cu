@@ -108,6 +108,7 @@ __device__ __forceinline__ void from_smem(double2 (&v)[1 << R], const double2* s
 struct OpCtx {
   double a, bb;    // new = a v + bb * (i^BI) * p   (bb carries the uniform part of the partner sign)
   double2 bc;      // generic complex b' (reverse mode 6)
+  uint32_t pneg;   // permutation modes: sign of bb (bb = +-1)
   uint32_t smask;  // register part of the partner sign (runtime patterns only)
   uint32_t cmask;  // register part of the control test
   bool clw_ok;     // lane/warp part of the control test
@@ -131,6 +132,10 @@ struct Pat {
 // v <- a v + (-1)^neg bb (i^BI p)      (in-place friendly: the DFMA overwrites v)
 template <int BI>
 __device__ __forceinline__ double2 upd(const OpCtx& c, double2 v, double2 p, bool neg) {
+  if (BI >= 3) {  // pure Pauli (a = 0, |b'| = 1): a signed permutation, no arithmetic
+    const uint32_t s = uint32_t(neg) ^ c.pneg;
+    return BI == 3 ? sflip(p, s) : sflip(make_double2(-p.y, p.x), s);
+  }
   double tx, ty;
   if (BI == 1) {
     tx = -c.bb * p.y;
@@ -224,20 +229,23 @@ __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], double2 (&l)[1 << R
 
 // Flat variant id (computed on the host, see engine.cu emit_rop):
 //   id = pattern + Pat<R>::N * (ctrl + 2 * mode)
-//   mode: 0/1 forward (BI 0/1); 2/3 reverse IPK 0 (BI 0/1); 4/5 reverse IPK 1 (BI 0/1);
-//         6 reverse IPK 3 (generic complex coefficients)
+//   mode: forward 0/1 (BI 0/1), 2/3 (signed permutation, BI 0/1: pure Pauli X/Y/Z, CX...);
+//         reverse 4/5 (IPK 1, BI 0/1), 6 (IPK 3, generic complex coefficients),
+//         7/8 (signed permutation on phi and lambda, BI 0/1)
+constexpr int kModes = 9;
 template <int R, int NB, int V>
 __device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
                                             double& q0, double& q1, double2& z, double2& z2) {
   constexpr int NP = Pat<R>::N;
-  if constexpr (V < NP * 2 * 7) {
+  if constexpr (V < NP * 2 * kModes) {
     constexpr int P = V % NP;
     constexpr bool CTRL = (V / NP) % 2;
     constexpr int mode = V / NP / 2;
-    constexpr bool DUAL = mode >= 2;
-    constexpr int IPK = mode >= 6 ? 3 : (mode >= 4 ? 1 : 0);
-    constexpr int BI = mode == 6 ? 2 : (mode & 1);
-    if constexpr (NB == 2 || !DUAL) reg_op<R, P, IPK, BI, CTRL, DUAL>(v, l, c, xl, q0, q1, z, z2);
+    constexpr bool DUAL = mode >= 4;
+    constexpr int IPK = mode == 6 ? 3 : ((mode == 4 || mode == 5) ? 1 : 0);
+    constexpr int BI = mode == 6 ? 2 : (mode == 2 || mode == 7) ? 3 : (mode == 3 || mode == 8) ? 4 : (mode & 1);
+    // forward kernels only hold forward modes, reverse kernels only reverse modes (code size)
+    if constexpr ((NB == 2) == DUAL) reg_op<R, P, IPK, BI, CTRL, DUAL>(v, l, c, xl, q0, q1, z, z2);
   }
 }
 
@@ -252,13 +260,14 @@ __device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1
 template <int R, int NB>
 __device__ __forceinline__ void dispatch(uint32_t id, double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c,
                                          uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
-  static_assert(Pat<R>::N * 2 * 7 <= 320, "extend the dispatch table");
+  static_assert(Pat<R>::N * 2 * kModes <= 384, "extend the dispatch table");
   switch (id) {
     SVGB_V64(0)
     SVGB_V64(64)
     SVGB_V64(128)
     SVGB_V64(192)
     SVGB_V64(256)
+    SVGB_V64(320)
     default:
       break;
   }
@@ -277,7 +286,7 @@ __device__ __forceinline__ double warp_sum1(double v) {
 }  // namespace
 
 template <int R, int NB>
-__global__ void __launch_bounds__(kRegThreads, R == 3 ? 2 : 1) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
+__global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3 ? 2 : (NB == 2 ? 2 : 4)) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
                                                              const PassDesc d, const SegDesc* __restrict__ segs,
                                                              const RegOp* __restrict__ rops,
                                                              const DevOp* __restrict__ ops,
@@ -345,6 +354,7 @@ __global__ void __launch_bounds__(kRegThreads, R == 3 ? 2 : 1) k_pass_reg(double
           c.smask = op.smask;
           c.cmask = op.cmask;
           c.clw_ok = (tbase & op.clw) == op.clw;
+          c.pneg = c.bb < 0.0;
           double q0 = 0.0, q1 = 0.0;
           double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
           dispatch<R, NB>(op.variant, v, l, c, op.xl, q0, q1, z, z2);
@@ -443,7 +453,7 @@ size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles, boo
   return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(RegOp) * nops + tacc;
 }
 
-int reg_max_threads() { return kRegThreads; }
+int reg_max_threads(int R) { return R == 3 ? kRegThreads : kRegThreads / 2; }
 
 cudaError_t prepare_reg_kernels(size_t max_smem) {
   for (int R = 3; R <= 4; ++R)

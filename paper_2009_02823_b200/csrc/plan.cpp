@@ -213,7 +213,7 @@ std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const 
 int choose_tile_qubits(int n, int requested, int sms) {
   if (requested > 0) return std::min(requested, n);
   if (n <= 10) return n;  // whole state in one tile: one CTA, no HBM round trips between passes
-  int k = std::min(n, 10);
+  int k = std::min(n, 11);
   // keep at least ~4 tiles per SM so the persistent grid stays balanced
   while (k > 9 && (n - k) < 62 && (1ll << (n - k)) < 4ll * sms) --k;
   return std::min(k, n);
