@@ -56,6 +56,8 @@ struct PassDesc {
   int32_t seg_begin, seg_end;  // register-tile passes: segment range
   int32_t smem_tiles;    // register-tile passes: 1 if the pass stages tiles in shared memory
   int32_t thread_acc;    // register-tile reverse passes: per-thread inner-product accumulators
+  int32_t prefetch;      // register-tile passes: stream tiles through shared memory with cp.async.bulk
+  int32_t pad1;
   uint8_t q[kMaxQubits]; // tile qubits ascending
 };
 

@@ -150,7 +150,7 @@ struct svg_engine {
   size_t max_smem = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4;
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4, opt_prefetch = 1;
   DeviceBuf psi, lam, partials, blob, results;
   HostBuf hblob, hres;
   cudaEvent_t ev[6] = {};
@@ -673,8 +673,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       case L_REG:
         // per-thread inner-product accumulators when they fit a modest budget
         l.d.thread_acc = l.nb == 2 && size_t(l.d.nslots) * l.threads * sizeof(double) <= (48u << 10);
-        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles,
-                          l.d.thread_acc != 0);
+        l.d.prefetch = e->opt_prefetch != 0;
+        l.smem = reg_smem(L.k, l.d.b, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles,
+                          l.d.thread_acc != 0, l.d.prefetch != 0);
         l.grid = clamp_grid(reg_occupancy(l.nb, l.R, l.threads, l.smem));
         break;
       case L_OBS:
@@ -963,6 +964,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     if (value == 0) value = 4;
     if (value != 3 && value != 4) return fail(SVG_EINVAL, k + " must be 3 or 4");
     (k == "reg_bits" ? e->opt_reg_bits : e->opt_reg_bits_fwd) = value;
+  } else if (k == "prefetch") {
+    e->opt_prefetch = value != 0;
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;

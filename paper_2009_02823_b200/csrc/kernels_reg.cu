@@ -40,6 +40,51 @@ __device__ __forceinline__ double2 sflip(double2 v, uint32_t s) {
                       __longlong_as_double(__double_as_longlong(v.y) ^ m));
 }
 
+// ---- async bulk copies (TMA engine, cp.async.bulk) completing on an mbarrier ----
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Warp 0 streams tile `base` (rows of 2^b contiguous amplitudes) into the stage buffers.
+template <int NB>
+__device__ __forceinline__ void prefetch_tile(const PassDesc& d, const uint64_t* rows, uint64_t base,
+                                              const double2* b0, const double2* b1, double2* st0, double2* st1,
+                                              uint64_t* bar) {
+  // one elected thread issues every row (the bulk-copy operands live in uniform registers)
+  if ((threadIdx.x & 31) != 0) return;
+  const int nrows = 1 << (d.k - d.b);
+  const uint32_t row_bytes = uint32_t(sizeof(double2)) << d.b;
+  fence_async_smem();  // order earlier generic-proxy smem accesses before the async writes
+  mbar_expect_tx(bar, uint32_t(NB) * uint32_t(nrows) * row_bytes);
+  for (int r = 0; r < nrows; ++r) {
+    const uint64_t g = base | rows[r];
+    bulk_g2s(st0 + (size_t(r) << d.b), b0 + g, row_bytes, bar);
+    if (NB == 2) bulk_g2s(st1 + (size_t(r) << d.b), b1 + g, row_bytes, bar);
+  }
+}
+
 template <int R>
 struct Map {
   uint64_t gw;        // global offset of this warp's warp bits
@@ -314,7 +359,20 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
     for (int i = threadIdx.x; i < nops * int(sizeof(RegOp) / 16); i += nthr) dst[i] = src[i];
   }
   if (threadIdx.x < kMaxQubits) sq[threadIdx.x] = d.q[threadIdx.x];
+  __shared__ uint64_t mbar;
+  uint64_t* rows = reinterpret_cast<uint64_t*>(st1 + (NB == 2 ? (1u << d.k) : 0));  // [2^(k-b)] row offsets
+  if (d.prefetch) {
+    for (int r = threadIdx.x; r < (1 << (d.k - d.b)); r += nthr) {
+      uint64_t off = 0;
+      for (int j = d.b; j < d.k; ++j)
+        if ((r >> (j - d.b)) & 1) off |= 1ull << d.q[j];
+      rows[r] = off;
+    }
+    if (threadIdx.x == 0) mbar_init(&mbar);
+  }
   __syncthreads();
+  if (d.prefetch && warp == 0) prefetch_tile<NB>(d, rows, pdep64(blockIdx.x, d.rest), b0, b1, st0, st1, &mbar);
+  uint32_t phase = 0;
 
   const uint32_t tbase = uint32_t(lane) | (uint32_t(warp) << (5 + R));
   double2 v[NR], l[NR];
@@ -323,13 +381,22 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   const uint64_t ntiles = 1ull << (d.n - d.k);
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
+    const uint64_t next = T + gridDim.x;
     Map<R> m;
     make_map<R>(m, segs[d.seg_begin], sq, warp, wbits);
-    load_g<R>(v, b0, base | lane | m.gw, m);
-    if (NB == 2) load_g<R>(l, b1, base | lane | m.gw, m);
+    if (d.prefetch) {  // this tile was streamed into the stage buffers by the async copy engine
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+      from_smem<R>(v, st0, lane | m.sw, m);
+      if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
+    } else {
+      load_g<R>(v, b0, base | lane | m.gw, m);
+      if (NB == 2) load_g<R>(l, b1, base | lane | m.gw, m);
+    }
     bool in_smem = false;
     for (int s = d.seg_begin; s < d.seg_end; ++s) {
       const SegDesc sg = segs[s];
+      const bool last = s + 1 == d.seg_end;
       if (sg.kind == SEG_REG) {
         if (s != d.seg_begin && (in_smem || !sg.same_map)) {
           if (!in_smem) {
@@ -342,6 +409,10 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
           from_smem<R>(v, st0, lane | m.sw, m);
           if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
           in_smem = false;
+        }
+        if (last && d.prefetch && next < ntiles) {  // stage buffers free: stream the next tile
+          __syncthreads();
+          if (warp == 0) prefetch_tile<NB>(d, rows, pdep64(next, d.rest), b0, b1, st0, st1, &mbar);
         }
         for (int o = sg.op_begin - d.op_begin; o < sg.op_end - d.op_begin; ++o) {
           const RegOp& op = sops[o];
@@ -401,6 +472,13 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
           }
           __syncthreads();
         }
+        if (last && d.prefetch) {
+          from_smem<R>(v, st0, lane | m.sw, m);
+          if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
+          in_smem = false;
+          __syncthreads();
+          if (warp == 0 && next < ntiles) prefetch_tile<NB>(d, rows, pdep64(next, d.rest), b0, b1, st0, st1, &mbar);
+        }
       }
     }
     if (in_smem) {
@@ -448,9 +526,11 @@ cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
 }
 }  // namespace
 
-size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, bool tiles, bool thread_acc) {
+size_t reg_smem(int k, int b, int nb, int nwarps, int nslots, int nops, bool tiles, bool thread_acc, bool prefetch) {
   const size_t tacc = thread_acc ? sizeof(double2) * ((size_t(nslots) * nwarps * 32 + 1) / 2) : 0;
-  return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(RegOp) * nops + tacc;
+  const size_t rows = prefetch ? sizeof(uint64_t) << (k - b) : 0;
+  return sizeof(double2) * (size_t(nwarps) * nslots + ((tiles || prefetch) ? (size_t(nb) << k) : 0)) +
+         sizeof(RegOp) * nops + tacc + rows;
 }
 
 int reg_max_threads(int R) { return R == 3 ? kRegThreads : kRegThreads / 2; }
