@@ -54,7 +54,7 @@ def _args():
     ap.add_argument("--tile-qubits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0, help="reverse register tile: 2^bits amplitudes/thread (3/4)")
     ap.add_argument("--reg-bits-fwd", type=int, default=0, help="forward register tile: 2^bits amplitudes/thread")
-    ap.add_argument("--no-prefetch", action="store_true", help="load tiles with plain loads instead of cp.async.bulk")
+    ap.add_argument("--prefetch", action="store_true", help="stream tiles with cp.async.bulk into shared memory")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -200,7 +200,7 @@ def run_ours(args, rank, world, local_rank):
         eng.set_option("reg_bits", args.reg_bits)
     if args.reg_bits_fwd:
         eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
-    eng.set_option("prefetch", 0 if args.no_prefetch else 1)
+    eng.set_option("prefetch", 1 if args.prefetch else 0)
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

@@ -150,7 +150,7 @@ struct svg_engine {
   size_t max_smem = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4, opt_prefetch = 1;
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4, opt_prefetch = 0;
   DeviceBuf psi, lam, partials, blob, results;
   HostBuf hblob, hres;
   cudaEvent_t ev[6] = {};
