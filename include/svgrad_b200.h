@@ -136,6 +136,9 @@ typedef struct {
   int64_t d2h_bytes;
   int32_t segments;          /* register-tile segments over all passes (0: shared-memory kernels) */
   int32_t reg_bits;          /* amplitudes per thread per buffer = 2^reg_bits (register kernels) */
+  int32_t swaps;             /* sharded engines: qubit swaps (rank bit <-> local qubit) per sweep */
+  int32_t reserved;
+  int64_t exchange_bytes;    /* sharded engines: bytes one shard sends to partners per sweep */
 } svg_stats;
 
 typedef struct svg_engine svg_engine;
@@ -145,6 +148,14 @@ const char* svg_last_error(void);   /* thread-local message of the last failure 
 int svg_device_count(int* out);
 
 int svg_engine_create(int device, svg_engine** out);
+/* Sharded engines: the state is split over `shards` (a power of two) by its
+ * top log2(shards) qubits.  A virtual engine holds every shard on one device
+ * (exercises the distributed schedule on one GPU); an NCCL engine is one rank
+ * of a one-process-per-GPU job (all ranks call it with the same unique id,
+ * from svg_nccl_unique_id on rank 0).  Results are complete on every rank. */
+int svg_engine_create_virtual(int device, int shards, svg_engine** out);
+int svg_nccl_unique_id(uint8_t id_out[128]);
+int svg_engine_create_sharded(int device, int world, int rank, const uint8_t nccl_id[128], svg_engine** out);
 int svg_engine_destroy(svg_engine* e);
 /* Launch on an external cudaStream_t (passed as void*); NULL = engine's own stream. */
 int svg_engine_set_stream(svg_engine* e, void* stream);
@@ -171,6 +182,15 @@ int svg_expectation(svg_engine* e, const svg_problem* p, svg_c128* energy_out, s
 int svg_plan_inspect(const svg_problem* p, int tile_qubits, int sms, int32_t* order_out,
                      int32_t* pass_start_out, uint64_t* qmask_out, int32_t* npasses_out,
                      int32_t* tile_qubits_out);
+
+/* Host-only sharded schedule (no CUDA calls) for `shards` shards: steps are
+ * passes (step_swap_out[j] == 0; gates order_out[step_start[j]..step_start[j+1]),
+ * tile qubits qmask_out[j] over physical local positions) or qubit swaps
+ * (step_swap_out[j] == ((gbit << 8) | lpos) + 1).  Arrays sized for
+ * num_gates + 2 * num_gates steps (an upper bound). */
+int svg_plan_schedule(const svg_problem* p, int shards, int tile_qubits, int sms, int32_t* order_out,
+                      int32_t* step_start_out, int32_t* step_swap_out, uint64_t* qmask_out, int32_t* nsteps_out,
+                      int32_t* tile_qubits_out);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,8 @@ FORM_PAULI, FORM_MAT = 0, 1
 EXPORTED = (
     "svg_abi_version", "svg_last_error", "svg_device_count", "svg_engine_create",
     "svg_engine_destroy", "svg_engine_set_stream", "svg_engine_set_option",
-    "svg_reverse_sweep", "svg_expectation", "svg_plan_inspect",
+    "svg_reverse_sweep", "svg_expectation", "svg_plan_inspect", "svg_engine_create_virtual",
+    "svg_nccl_unique_id", "svg_engine_create_sharded", "svg_plan_schedule",
 )
 
 
@@ -74,6 +75,7 @@ class svg_stats(C.Structure):
         ("fwd_passes", C.c_int32), ("obs_passes", C.c_int32), ("rev_passes", C.c_int32),
         ("tile_qubits", C.c_int32), ("pass_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64), ("segments", C.c_int32), ("reg_bits", C.c_int32),
+        ("swaps", C.c_int32), ("reserved", C.c_int32), ("exchange_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -112,6 +114,13 @@ def load(path: str = LIB_PATH):
             C.POINTER(svg_problem), C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
             C.POINTER(C.c_int32), C.POINTER(C.c_int32),
         ]
+        lib.svg_plan_schedule.argtypes = [
+            C.POINTER(svg_problem), C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+        ]
+        lib.svg_engine_create_virtual.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        lib.svg_nccl_unique_id.argtypes = [C.c_void_p]
+        lib.svg_engine_create_sharded.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
         for name in EXPORTED:
             getattr(lib, name).restype = C.c_char_p if name == "svg_last_error" else C.c_int
         if lib.svg_abi_version() != ABI_VERSION:
@@ -142,12 +151,23 @@ class Engine:
     for the duration of the native call.
     """
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, *, shards: int = 1, rank: int | None = None,
+                 nccl_id: bytes | None = None):
+        """shards == 1: one device, whole state.  shards > 1 and rank None: virtual
+        shards on this device.  rank given: one rank of a `shards`-GPU NCCL job."""
         self.lib = load()
         handle = C.c_void_p()
-        check(self.lib.svg_engine_create(int(device), C.byref(handle)))
+        if shards == 1 and rank is None:
+            check(self.lib.svg_engine_create(int(device), C.byref(handle)))
+        elif rank is None:
+            check(self.lib.svg_engine_create_virtual(int(device), int(shards), C.byref(handle)))
+        else:
+            buf = C.create_string_buffer(bytes(nccl_id or b""), 128)
+            check(self.lib.svg_engine_create_sharded(int(device), int(shards), int(rank), buf, C.byref(handle)))
         self.handle = handle
         self.device = device
+        self.shards = shards
+        self.rank = rank
         self.lock = threading.Lock()
 
     def set_option(self, key: str, value: int) -> None:
@@ -199,6 +219,38 @@ def plan_inspect(problem: svg_problem, tile_qubits: int = 0, sms: int = 0):
                                start.ctypes.data, qmask.ctypes.data, C.byref(npasses), C.byref(k)))
     m = npasses.value
     return order[: problem.num_gates], start[: m + 1], qmask[:m], k.value
+
+
+def nccl_unique_id() -> bytes:
+    lib = load()
+    buf = C.create_string_buffer(128)
+    check(lib.svg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def plan_schedule(problem: svg_problem, shards: int, tile_qubits: int = 0, sms: int = 0):
+    """Sharded schedule without a GPU: list of ('pass', gate_indices, qmask) / ('swap', gbit, lpos)."""
+    import numpy as np
+
+    lib = load()
+    G = max(1, problem.num_gates)
+    cap = G * (2 * max(1, shards).bit_length() + 3) + 8
+    order = np.zeros(G, dtype=np.int32)
+    start = np.zeros(cap + 1, dtype=np.int32)
+    swap = np.zeros(cap, dtype=np.int32)
+    qmask = np.zeros(cap, dtype=np.uint64)
+    nsteps, k = C.c_int32(), C.c_int32()
+    check(lib.svg_plan_schedule(C.byref(problem), int(shards), int(tile_qubits), int(sms), order.ctypes.data,
+                                start.ctypes.data, swap.ctypes.data, qmask.ctypes.data, C.byref(nsteps),
+                                C.byref(k)))
+    steps = []
+    for j in range(nsteps.value):
+        if swap[j]:
+            code = int(swap[j]) - 1
+            steps.append(("swap", code >> 8, code & 0xFF))
+        else:
+            steps.append(("pass", order[start[j]:start[j + 1]].tolist(), int(qmask[j])))
+    return steps, k.value
 
 
 _engines: dict[int, Engine] = {}

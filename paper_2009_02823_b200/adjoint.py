@@ -88,14 +88,15 @@ def _account(counters, audit, num_gates: int, num_derivs: int) -> None:
 
 
 def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, stats: dict | None = None,
-          real_sums: bool = False):
+          real_sums: bool = False, engine=None):
     """Equivalent of the reference's ``_reverse_sweep``: (complex sums[P], energy).
 
     ``real_sums=True`` lets the engine skip Im(sums) (returned as 0) when the
     caller only forms 2*Re, as the Hermitian path does (svgrad/gradients.py:198).
     """
     problem = Problem(circuit, params, obs, input_state, real_sums=real_sums)
-    sums, _, energy, st = _native.engine(device).reverse_sweep(problem.c, circuit.num_params, problem.num_derivs)
+    eng = engine or _native.engine(device)
+    sums, _, energy, st = eng.reverse_sweep(problem.c, circuit.num_params, problem.num_derivs)
     _account(counters, audit, len(circuit.gates), problem.num_derivs)
     out = np.ctypeslib.as_array(sums).view(np.complex128)[: circuit.num_params].copy()
     if stats is not None:
@@ -104,30 +105,35 @@ def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, s
 
 
 def reverse_mode_gradient(circuit, params, obs, input_state, audit: LiveStateAudit | None = None,
-                          *, device: int = 0, stats: dict | None = None) -> GradientReport:
-    """Full gradient of a Hermitian expectation in one fused backward sweep on the GPU."""
+                          *, device: int = 0, stats: dict | None = None, engine=None) -> GradientReport:
+    """Full gradient of a Hermitian expectation in one fused backward sweep on the GPU.
+
+    ``engine``: a specific ``_native.Engine`` (e.g. a sharded one from
+    ``paper_2009_02823_b200.distributed``); default: the process engine of ``device``.
+    """
     if not is_hermitian(obs):
         raise ValueError(_HERMITIAN_MSG)
     params = _check_call(circuit, params, obs, input_state)
     counters = OpCounters()
     sums, energy = sweep(circuit, params, obs, input_state, counters, audit or LiveStateAudit(), device, stats,
-                         real_sums=True)
+                         real_sums=True, engine=engine)
     return GradientReport((2.0 * sums.real).astype(complex), energy, counters)
 
 
-def non_hermitian_gradient(circuit, params, obs, input_state, *, device: int = 0) -> GradientReport:
+def non_hermitian_gradient(circuit, params, obs, input_state, *, device: int = 0, engine=None) -> GradientReport:
     """Complex gradient of <psi|A|psi>: A-sweep conjugated plus A^dag-sweep (svgrad/gradients.py:240-259)."""
     params = _check_call(circuit, params, obs, input_state)
     counters = OpCounters()
     audit = LiveStateAudit()
-    sums_a, energy = sweep(circuit, params, obs, input_state, counters, audit, device)
-    sums_adj, _ = sweep(circuit, params, adjoint_observable(obs), input_state, counters, audit, device)
+    sums_a, energy = sweep(circuit, params, obs, input_state, counters, audit, device, engine=engine)
+    sums_adj, _ = sweep(circuit, params, adjoint_observable(obs), input_state, counters, audit, device,
+                        engine=engine)
     return GradientReport(np.conj(sums_a) + sums_adj, energy, counters)
 
 
-def circuit_expectation(circuit, params, obs, input_state, *, device: int = 0) -> complex:
+def circuit_expectation(circuit, params, obs, input_state, *, device: int = 0, engine=None) -> complex:
     """<psi(theta)|H|psi(theta)> via the forward passes and the observable kernel only."""
     params = _check_call(circuit, params, obs, input_state)
     problem = Problem(circuit, params, obs, input_state)
-    energy, _ = _native.engine(device).expectation(problem.c)
+    energy, _ = (engine or _native.engine(device)).expectation(problem.c)
     return complex(energy.re, energy.im)

@@ -58,6 +58,12 @@ struct PassDesc {
   int32_t thread_acc;    // register-tile reverse passes: per-thread inner-product accumulators
   int32_t prefetch;      // register-tile passes: stream tiles through shared memory with cp.async.bulk
   int32_t pad1;
+  // Sharded state: this shard's rank bits in the physical amplitude index
+  // (ORed into the tile base for Z-signs and controls, never for addressing),
+  // and for observable passes the flip pattern on the rank bits of the source
+  // shard (the partner whose amplitudes feed lambda).
+  uint64_t rank_bits;
+  uint64_t xglob;
   uint8_t q[kMaxQubits]; // tile qubits ascending
 };
 

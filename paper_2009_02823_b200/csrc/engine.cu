@@ -25,6 +25,7 @@
 #include "../../include/svgrad_b200.h"
 #include "device.cuh"
 #include "kernels.h"
+#include "nccl_shim.h"
 #include "plan.h"
 
 using namespace svgb;
@@ -105,7 +106,7 @@ struct HostBuf {
   }
 };
 
-enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG };
+enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG, L_SWAP, L_FETCH };
 
 struct Launch {
   PassDesc d;
@@ -116,11 +117,14 @@ struct Launch {
   int threads = kThreads;
   int R = 3;           // L_REG: register bits
   bool tiles = false;  // L_REG: stages the tile through shared memory
+  int gbit = 0, lpos = 0;  // L_SWAP: rank bit <-> local position
 };
 
 // Everything a sweep needs on the host side, built from one svg_problem.
 struct Lowered {
-  int n = 0, k = 0, b = 0;
+  int n = 0, nloc = 0, k = 0, b = 0;
+  int swaps = 0, obs_kernels = 0;
+  int64_t swap_bytes = 0;  // bytes each shard exchanges (swaps both ways + partner fetches)
   bool reg = false;  // register-tile kernels in use
   int R = 3;         // their register bits
   std::vector<DevOp> ops;
@@ -151,8 +155,15 @@ struct svg_engine {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4, opt_prefetch = 0;
-  DeviceBuf psi, lam, partials, blob, results;
+  DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
+  // sharding: the state is split over 2^shard_bits shards by its top physical
+  // qubits; this engine holds `shards_local` of them (virtual shards on one
+  // device), or exactly one (rank `rank` of an NCCL communicator)
+  int shard_bits = 0;
+  int shards_local = 1;
+  int rank = 0;
+  NcclComm comm = nullptr;
   cudaEvent_t ev[6] = {};
 };
 
@@ -439,13 +450,28 @@ bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
   return __builtin_popcount(hi) == 1 && (flip_tile & 31u) == 0;
 }
 
+// Physical copy of a gate under the logical -> physical qubit map of its step.
+svg_gate physical_gate(const svg_gate& g, const std::vector<int>& l2p) {
+  svg_gate q = g;
+  for (int j = 0; j < g.ntargets; ++j) q.targets[j] = l2p[g.targets[j]];
+  q.ctrl_mask = remap_mask(g.ctrl_mask, l2p);
+  q.x_mask = remap_mask(g.x_mask, l2p);
+  q.z_mask = remap_mask(g.z_mask, l2p);
+  return q;
+}
+
 Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   Lowered L;
   const int n = p->num_qubits;
+  const int g = e->shard_bits;  // log2(shards): top g physical qubits select the shard
+  const int nloc = n - g;
+  if (nloc < 1) throw InvalidArg("more shards than amplitudes");
   const bool real_sums = (p->flags & SVG_FLAG_REAL_SUMS) != 0;
   L.n = n;
-  L.k = choose_tile_qubits(n, static_cast<int>(e->opt_tile), e->sms);
-  L.b = (n <= L.k) ? n : std::min(5, L.k - 2);
+  L.nloc = nloc;
+  L.k = choose_tile_qubits(nloc, static_cast<int>(e->opt_tile), e->sms);
+  L.b = (nloc <= L.k) ? nloc : std::min(5, L.k - 2);
+  if (g > 0 && L.b < 5 && nloc > L.k) throw InvalidArg("sharded engines need >= 7 qubits per shard");
   const int RB = static_cast<int>(e->opt_reg_bits);      // reverse passes
   const int RF = static_cast<int>(e->opt_reg_bits_fwd);  // forward passes
   L.R = RB;
@@ -453,15 +479,26 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   L.reg = e->opt_kernel != 1 && L.b >= 5 && fits(RB) && fits(RF);
   if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 5 + reg_bits .. 13 tile qubits");
   PlanParams pp;
-  pp.n = n;
+  pp.n = nloc;
   pp.k = L.k;
   pp.b = L.b;
   if (e->opt_max_items > 0) pp.max_items = static_cast<int>(e->opt_max_items);
-  const int64_t S = int64_t(16) << n;
+  const int64_t S = int64_t(16) << nloc;  // bytes of one state shard
 
-  std::vector<GateShape> shapes(p->num_gates);
-  for (int i = 0; i < p->num_gates; ++i) shapes[i] = gate_shape(p->gates[i]);
-  const std::vector<Pass> gpasses = plan_gate_passes(shapes, pp);
+  std::vector<GateShape> logical(p->num_gates);
+  for (int i = 0; i < p->num_gates; ++i) logical[i] = gate_shape(p->gates[i]);
+  std::vector<int> l2p_final;
+  const std::vector<Step> steps = plan_schedule(logical, n, g, pp, &l2p_final);
+  // physical gates per pass step, parallel to the step's items
+  std::vector<std::vector<svg_gate>> pgates(steps.size());
+  std::vector<std::vector<GateShape>> pshapes(steps.size());
+  for (size_t si = 0; si < steps.size(); ++si) {
+    if (steps[si].swap) continue;
+    for (int gi : steps[si].pass.items) {
+      pgates[si].push_back(physical_gate(p->gates[gi], steps[si].l2p));
+      pshapes[si].push_back(gate_shape(pgates[si].back()));
+    }
+  }
 
   std::vector<int> first_deriv(p->num_gates + 1, 0);
   for (int i = 0; i < p->num_gates; ++i) first_deriv[i + 1] = first_deriv[i] + p->gates[i].nderiv;
@@ -469,26 +506,26 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   for (int d = 0; d < p->num_derivs; ++d) gens[d] = make_gen(p->gates[p->derivs[d].gate], p->derivs[d]);
 
   // segments per pass (register path)
-  std::vector<std::vector<Segment>> psegs(gpasses.size()), psegs_f(gpasses.size());
+  std::vector<std::vector<Segment>> psegs(steps.size()), psegs_f(steps.size());
   if (L.reg) {
-    for (size_t pi = 0; pi < gpasses.size(); ++pi) {
-      const Pass& ps = gpasses[pi];
+    for (size_t si = 0; si < steps.size(); ++si) {
+      if (steps[si].swap) continue;
+      const Pass& ps = steps[si].pass;
       const TileMap tm = tile_map(ps.qmask);
       std::vector<uint32_t> flips(ps.items.size()), touch(ps.items.size());
       std::vector<char> dense(ps.items.size());
       for (size_t j = 0; j < ps.items.size(); ++j) {
-        const svg_gate& g = p->gates[ps.items[j]];
-        flips[j] = tm.local(shapes[ps.items[j]].flip);
-        touch[j] = tm.local(shapes[ps.items[j]].touch);
-        dense[j] = !reg_capable(g, flips[j]);
+        flips[j] = tm.local(pshapes[si][j].flip);
+        touch[j] = tm.local(pshapes[si][j].touch);
+        dense[j] = !reg_capable(pgates[si][j], flips[j]);
       }
-      psegs[pi] = plan_segments(flips, touch, dense, L.k, RB);
-      psegs_f[pi] = RF == RB ? psegs[pi] : plan_segments(flips, touch, dense, L.k, RF);
+      psegs[si] = plan_segments(flips, touch, dense, L.k, RB);
+      psegs_f[si] = RF == RB ? psegs[si] : plan_segments(flips, touch, dense, L.k, RF);
     }
   }
   auto reg_launch = [&](const Pass& ps, int nb) {
     Launch l;
-    l.d = make_desc(n, L.k, ps.qmask);
+    l.d = make_desc(nloc, L.k, ps.qmask);
     l.kind = L_REG;
     l.nb = nb;
     l.R = nb == 1 ? RF : RB;
@@ -497,39 +534,49 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     l.d.op_begin = static_cast<int>(L.rops.size());  // this pass's register ops (staged in smem)
     return l;
   };
+  auto swap_launch = [&](const Step& st) {
+    Launch l;
+    l.kind = L_SWAP;
+    l.gbit = st.gbit;
+    l.lpos = st.lpos;
+    return l;
+  };
   // default register layout for shared-memory segments: lowest non-lane positions
   auto default_regs = [](int R) { return ((1u << (5 + R)) - 1u) & ~31u; };
 
-  // forward passes
-  for (size_t pi = 0; pi < gpasses.size(); ++pi) {
-    const Pass& ps = gpasses[pi];
+  // forward schedule
+  for (size_t si = 0; si < steps.size(); ++si) {
+    if (steps[si].swap) {
+      L.fwd.push_back(swap_launch(steps[si]));
+      L.swap_bytes += S;  // half a shard out, half in
+      continue;
+    }
+    const Pass& ps = steps[si].pass;
+    const std::vector<svg_gate>& gs = pgates[si];
     const TileMap tm = tile_map(ps.qmask);
     if (!L.reg) {
       Launch l;
-      l.d = make_desc(n, L.k, ps.qmask);
+      l.d = make_desc(nloc, L.k, ps.qmask);
       l.kind = L_SMEM_FWD;
       l.d.op_begin = static_cast<int>(L.ops.size());
-      for (int gi : ps.items) emit_op(L, tm, p->gates[gi], OP_APPLY_PAULI, 0, p->gates[gi].fwd, 0);
+      for (const svg_gate& gt : gs) emit_op(L, tm, gt, OP_APPLY_PAULI, 0, gt.fwd, 0);
       l.d.op_end = static_cast<int>(L.ops.size());
       L.fwd.push_back(l);
     } else {
       Launch l = reg_launch(ps, 1);
       uint32_t prev = ~0u;
-      for (const Segment& sg : psegs_f[pi]) {
+      for (const Segment& sg : psegs_f[si]) {
         SegLocal sl;
         SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF), L.k, RF, &sl);
         sd.same_map = sg.reg && sg.regmask == prev;
         prev = sg.reg ? sg.regmask : ~0u;
         if (sg.reg) {
           sd.op_begin = static_cast<int>(L.rops.size());
-          for (int it : sg.items) {
-            const svg_gate& g = p->gates[ps.items[it]];
-            emit_rop(L, tm, sl, g, ROP_FWD, g.fwd, nullptr, 0, real_sums);
-          }
+          for (int it : sg.items) emit_rop(L, tm, sl, gs[it], ROP_FWD, gs[it].fwd, nullptr, 0, real_sums);
           sd.op_end = static_cast<int>(L.rops.size());
         } else {
           sd.op_begin = static_cast<int>(L.ops.size());
-          for (int it : sg.items) emit_op(L, tm, p->gates[ps.items[it]], OP_APPLY_PAULI, 0, p->gates[ps.items[it]].fwd, 0);
+          for (int it : sg.items) emit_op(L, tm, gs[it], OP_APPLY_PAULI, 0, gs[it].fwd, 0);
           sd.op_end = static_cast<int>(L.ops.size());
           l.tiles = true;
         }
@@ -537,82 +584,119 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
       l.d.seg_end = static_cast<int>(L.segs.size());
       l.d.op_end = static_cast<int>(L.rops.size());
-      if (psegs_f[pi].size() > 1) l.tiles = true;
+      if (psegs_f[si].size() > 1) l.tiles = true;
       L.fwd.push_back(l);
     }
     L.pass_bytes += 2 * S;
   }
 
-  // observable passes (terms grouped by flip mask into tiles)
-  std::vector<uint64_t> flips(p->num_terms);
-  for (int t = 0; t < p->num_terms; ++t) flips[t] = p->terms[t].x_mask;
-  std::vector<int> direct;
-  std::vector<Pass> tpasses = plan_term_passes(flips, pp, &direct);
-  if (!direct.empty()) {  // wide flip masks: one untiled gather pass (qmask 0)
-    Pass ps;
-    ps.items = direct;
-    tpasses.push_back(ps);
+  // observable passes: terms in the final physical layout, grouped by the flip
+  // pattern on rank bits (a nonzero pattern reads the partner shard's psi), then
+  // by local flip mask into tiles
+  const uint64_t loc_mask = (nloc >= 64) ? ~0ull : ((1ull << nloc) - 1);
+  std::vector<uint64_t> xg_order;
+  std::vector<std::vector<int>> by_xg;
+  std::vector<svg_pauli_term> pterms(p->num_terms);
+  for (int t = 0; t < p->num_terms; ++t) {
+    pterms[t] = p->terms[t];
+    pterms[t].x_mask = remap_mask(p->terms[t].x_mask, l2p_final);
+    pterms[t].z_mask = remap_mask(p->terms[t].z_mask, l2p_final);
+    const uint64_t xg = pterms[t].x_mask & ~loc_mask;
+    size_t j = 0;
+    while (j < xg_order.size() && xg_order[j] != xg) ++j;
+    if (j == xg_order.size()) {
+      xg_order.push_back(xg);
+      by_xg.emplace_back();
+    }
+    by_xg[j].push_back(t);
   }
   int64_t part = 0;
   const int64_t energy_off = 0;
-  for (size_t j = 0; j < tpasses.size(); ++j) {
-    const Pass& ps = tpasses[j];
-    const TileMap tm = tile_map(ps.qmask);
-    Launch l;
-    l.d = make_desc(n, L.k, ps.qmask);
-    l.d.op_begin = static_cast<int>(L.terms.size());
-    l.d.untiled = ps.qmask == 0;
-    l.kind = l.d.untiled ? L_OBS_DIRECT : L_OBS;
-    for (int ti : ps.items) {
-      const svg_pauli_term& src = p->terms[ti];
-      DevTerm dt;
-      dt.c = cm(d2(src.coeff), ipow(src.n_y));
-      if (l.d.untiled) {  // full masks: x split over (xl, zl), z in zo
-        dt.xl = static_cast<uint32_t>(src.x_mask);
-        dt.zl = static_cast<uint32_t>(src.x_mask >> 32);
-        dt.zo = src.z_mask;
-      } else {
-        dt.xl = tm.local(src.x_mask);
-        dt.zl = tm.local(src.z_mask);
-        dt.zo = src.z_mask & ~tm.qmask;
-      }
-      L.terms.push_back(dt);
+  for (size_t gidx = 0; gidx < xg_order.size(); ++gidx) {
+    const uint64_t xg = xg_order[gidx];
+    const std::vector<int>& members = by_xg[gidx];
+    std::vector<uint64_t> flips(members.size());
+    for (size_t j = 0; j < members.size(); ++j) flips[j] = pterms[members[j]].x_mask & loc_mask;
+    std::vector<int> direct;
+    std::vector<Pass> tpasses = plan_term_passes(flips, pp, &direct);
+    if (!direct.empty()) {  // wide flip masks: one untiled gather pass (qmask 0)
+      Pass ps;
+      ps.items = direct;
+      tpasses.push_back(ps);
     }
-    l.d.op_end = static_cast<int>(L.terms.size());
-    l.d.accumulate = j > 0;
-    L.obs.push_back(l);
-    L.pass_bytes += (j > 0 ? 3 : 2) * S;
+    if (xg) L.obs.push_back(Launch{});  // exchange step: fetch the partner shard's psi
+    if (xg) {
+      L.obs.back().kind = L_FETCH;
+      L.obs.back().d.xglob = xg;
+      L.swap_bytes += 2 * S;
+    }
+    for (const Pass& ps : tpasses) {
+      const TileMap tm = tile_map(ps.qmask);
+      Launch l;
+      l.d = make_desc(nloc, L.k, ps.qmask);
+      l.d.op_begin = static_cast<int>(L.terms.size());
+      l.d.untiled = ps.qmask == 0;
+      l.d.xglob = xg;
+      l.kind = l.d.untiled ? L_OBS_DIRECT : L_OBS;
+      for (int ti : ps.items) {
+        const svg_pauli_term& src = pterms[members[ti]];
+        DevTerm dt;
+        dt.c = cm(d2(src.coeff), ipow(src.n_y));
+        const uint64_t xl = src.x_mask & loc_mask;
+        if (l.d.untiled) {  // local flip mask split over (xl, zl); full z in zo
+          dt.xl = static_cast<uint32_t>(xl);
+          dt.zl = static_cast<uint32_t>(xl >> 32);
+          dt.zo = src.z_mask;
+        } else {
+          dt.xl = tm.local(xl);
+          dt.zl = tm.local(src.z_mask);
+          dt.zo = src.z_mask & ~tm.qmask;
+        }
+        L.terms.push_back(dt);
+      }
+      l.d.op_end = static_cast<int>(L.terms.size());
+      l.d.accumulate = L.obs_kernels > 0;
+      L.obs_kernels++;
+      L.obs.push_back(l);
+      L.pass_bytes += (l.d.accumulate ? 3 : 2) * S;
+    }
   }
 
-  // reverse passes: forward passes backwards, gates backwards inside
-  std::vector<std::pair<int, int>> deriv_slot(p->num_derivs, {-1, -1});  // (rev pass, slot)
-  auto smem_reverse_ops = [&](const TileMap& tm, int gi, uint32_t& slot) {
-    const svg_gate& g = p->gates[gi];
-    emit_op(L, tm, g, OP_APPLY_PAULI, 0, g.rewind, 0);
-    for (int j = 0; j < g.nderiv; ++j) {
+  // reverse schedule: steps backwards (swaps undo themselves on phi and lambda),
+  // gates backwards inside each pass
+  std::vector<std::pair<int, int>> deriv_slot(p->num_derivs, {-1, -1});  // (rev launch, slot)
+  auto smem_reverse_ops = [&](const TileMap& tm, const svg_gate& gt, int gi, uint32_t& slot) {
+    emit_op(L, tm, gt, OP_APPLY_PAULI, 0, gt.rewind, 0);
+    for (int j = 0; j < gt.nderiv; ++j) {
       const int d = first_deriv[gi] + j;
       deriv_slot[d] = {static_cast<int>(L.rev.size()), static_cast<int>(slot)};
-      emit_op(L, tm, g, OP_IP_PAULI, 0, gens[d].pre, slot++);
+      emit_op(L, tm, gt, OP_IP_PAULI, 0, gens[d].pre, slot++);
     }
-    if (gi > 0) emit_op(L, tm, g, OP_APPLY_PAULI, 1, g.adjoint, 0);
+    if (gi > 0) emit_op(L, tm, gt, OP_APPLY_PAULI, 1, gt.adjoint, 0);
   };
   if (with_reverse) {
-    for (int pi = static_cast<int>(gpasses.size()) - 1; pi >= 0; --pi) {
-      const Pass& ps = gpasses[pi];
+    for (int si = static_cast<int>(steps.size()) - 1; si >= 0; --si) {
+      if (steps[si].swap) {
+        L.rev.push_back(swap_launch(steps[si]));
+        L.swap_bytes += 2 * S;
+        continue;
+      }
+      const Pass& ps = steps[si].pass;
+      const std::vector<svg_gate>& gs = pgates[si];
       const TileMap tm = tile_map(ps.qmask);
       uint32_t slot = 0;
       if (!L.reg) {
         Launch l;
-        l.d = make_desc(n, L.k, ps.qmask);
+        l.d = make_desc(nloc, L.k, ps.qmask);
         l.kind = L_SMEM_REV;
         l.d.op_begin = static_cast<int>(L.ops.size());
-        for (auto it = ps.items.rbegin(); it != ps.items.rend(); ++it) smem_reverse_ops(tm, *it, slot);
+        for (int j = static_cast<int>(ps.items.size()) - 1; j >= 0; --j) smem_reverse_ops(tm, gs[j], ps.items[j], slot);
         l.d.op_end = static_cast<int>(L.ops.size());
         l.d.nslots = static_cast<int>(slot);
         L.rev.push_back(l);
       } else {
         Launch l = reg_launch(ps, 2);
-        const std::vector<Segment>& sgs = psegs[pi];
+        const std::vector<Segment>& sgs = psegs[si];
         uint32_t prev = ~0u;
         for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
           const Segment& sg = *st;
@@ -624,21 +708,22 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
             sd.op_begin = static_cast<int>(L.rops.size());
             for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it) {
               const int gi = ps.items[*it];
-              const svg_gate& g = p->gates[gi];
+              const svg_gate& gt = gs[*it];
               const svg_c128* kpost = nullptr;
-              if (g.nderiv == 1) {
+              if (gt.nderiv == 1) {
                 const int d = first_deriv[gi];
                 deriv_slot[d] = {static_cast<int>(L.rev.size()), static_cast<int>(slot)};
                 kpost = gens[d].post;
               }
               // one op rewinds phi AND lambda (rewind == adjoint for register-capable gates);
               // the reference skips lambda's update at i = 0, whose value is never read again
-              emit_rop(L, tm, sl, g, ROP_REV, g.rewind, kpost, kpost ? slot++ : 0, real_sums);
+              emit_rop(L, tm, sl, gt, ROP_REV, gt.rewind, kpost, kpost ? slot++ : 0, real_sums);
             }
             sd.op_end = static_cast<int>(L.rops.size());
           } else {
             sd.op_begin = static_cast<int>(L.ops.size());
-            for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it) smem_reverse_ops(tm, ps.items[*it], slot);
+            for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it)
+              smem_reverse_ops(tm, gs[*it], ps.items[*it], slot);
             sd.op_end = static_cast<int>(L.ops.size());
             l.tiles = true;
           }
@@ -655,7 +740,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   }
 
   // grids, shared memory, partial offsets
-  const int64_t ntiles = int64_t(1) << (n - L.k);
+  const int64_t ntiles = int64_t(1) << (nloc - L.k);
   auto clamp_grid = [&](int per_sm) {
     const int64_t slots = int64_t(e->sms) * per_sm;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, slots)));
@@ -682,21 +767,27 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         l.smem = obs_smem(L.k, l.d.b);
         l.grid = clamp_grid(occupancy(1, l.smem));
         break;
-      default:
+      case L_OBS_DIRECT:
         l.smem = 0;
-        l.grid = std::max(1, static_cast<int>(std::min<int64_t>(int64_t(e->sms) * 8, int64_t(1) << std::max(0, n - 8))));
+        l.grid = std::max(1, static_cast<int>(std::min<int64_t>(int64_t(e->sms) * 8, int64_t(1) << std::max(0, nloc - 8))));
+        break;
+      default:  // exchanges: no kernel grid of their own
+        l.smem = 0;
+        l.grid = 0;
     }
     if (l.smem > e->max_smem) throw InvalidArg("pass needs more shared memory than the device offers");
   };
   for (Launch& l : L.fwd) size_launch(l);
   for (Launch& l : L.obs) {
     size_launch(l);
+    if (l.kind == L_FETCH) continue;
     l.d.part_off = part;
     part += l.grid;
   }
   const int64_t energy_count = part - energy_off;
   for (Launch& l : L.rev) {
     size_launch(l);
+    if (l.kind == L_SWAP) continue;
     l.d.part_off = part;
     part += int64_t(l.d.nslots) * l.grid;
   }
@@ -711,6 +802,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     L.sums.resize(1);
   }
   L.sums.back() = SumSpec{energy_off, energy_count};
+  for (const Step& st : steps) L.swaps += st.swap;
   return L;
 }
 
@@ -743,6 +835,14 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// One shard-local pass launch (sh: index of the shard held by this engine).
+struct ShardView {
+  double2* psi;
+  double2* lam;
+  double2* part;
+  uint64_t rank_bits;
+};
+
 int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_out,
         svg_c128* deriv_out, svg_c128* energy_out, svg_stats* stats) {
   if (!e) return fail(SVG_EINVAL, "null engine");
@@ -750,18 +850,26 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     validate(p);
     CK(cudaSetDevice(e->device));
     const Lowered L = lower(e, p, with_reverse);
-    const int n = L.n;
-    const size_t amps = size_t(1) << n;
+    const int nloc = L.nloc;
+    const int nsh = e->shards_local;       // shards held by this engine
+    const size_t shard_amps = size_t(1) << nloc;
+    const size_t amps = shard_amps * nsh;  // amplitudes held on this device
+    const int64_t cnt = static_cast<int64_t>(L.sums.size());
+    const int world = 1 << e->shard_bits;
     cudaStream_t s = e->stream;
 
     e->psi.reserve(amps * sizeof(double2));
     e->lam.reserve(amps * sizeof(double2));
-    e->partials.reserve(std::max<int64_t>(1, L.partial_count) * sizeof(double2));
+    e->partials.reserve(std::max<int64_t>(1, L.partial_count) * nsh * sizeof(double2));
     const Blob bl = layout(L);
     e->blob.reserve(bl.total);
     e->hblob.reserve(bl.total);
-    e->results.reserve(L.sums.size() * sizeof(double2));
-    e->hres.reserve(L.sums.size() * sizeof(double2));
+    e->results.reserve(cnt * std::max(nsh, world) * sizeof(double2));
+    e->hres.reserve(cnt * std::max(nsh, world) * sizeof(double2));
+    if (e->comm) {
+      e->scratch.reserve(shard_amps * sizeof(double2));
+      e->gathered.reserve(cnt * world * sizeof(double2));
+    }
 
     char* hb = static_cast<char*>(e->hblob.ptr);
     char* db = static_cast<char*>(e->blob.ptr);
@@ -777,6 +885,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     double2* psi = static_cast<double2*>(e->psi.ptr);
     double2* lam = static_cast<double2*>(e->lam.ptr);
     double2* part = static_cast<double2*>(e->partials.ptr);
+    double2* scratch = static_cast<double2*>(e->scratch.ptr);
     const DevOp* dops = reinterpret_cast<const DevOp*>(db + bl.ops);
     const double2* dcoef = reinterpret_cast<const double2*>(db + bl.coef);
     const DevTerm* dterms = reinterpret_cast<const DevTerm*>(db + bl.terms);
@@ -785,52 +894,139 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     const SegDesc* dsegs = reinterpret_cast<const SegDesc*>(db + bl.segs);
     double2* dres = static_cast<double2*>(e->results.ptr);
 
-    int64_t launches = 0, h2d = bl.total, d2h = L.sums.size() * sizeof(double2);
+    auto view = [&](int sh) {
+      const int rank = e->comm ? e->rank : sh;
+      return ShardView{psi + sh * shard_amps, lam + sh * shard_amps, part + sh * std::max<int64_t>(1, L.partial_count),
+                       uint64_t(rank) << nloc};
+    };
+    const Nccl* nccl = e->comm ? &Nccl::get() : nullptr;
+    const size_t half_bytes = shard_amps / 2 * sizeof(double2);
+    // rank bit `gbit` <-> local position `lpos` for one state buffer (see plan.h)
+    auto swap_buffer = [&](double2* buf, int gbit, int lpos) {
+      if (!e->comm) {
+        launch_swap_virtual(buf, nloc, nsh, gbit, lpos, s);
+        return;
+      }
+      const int a = (e->rank >> gbit) & 1, partner = e->rank ^ (1 << gbit);
+      double2* send = scratch;
+      double2* recv = scratch + shard_amps / 2;
+      launch_half_pack(buf, send, nloc, lpos, 1 - a, s);
+      nccl->check(nccl->group_start(), "ncclGroupStart");
+      nccl->check(nccl->send(send, half_bytes, kNcclUint8, partner, e->comm, s), "ncclSend");
+      nccl->check(nccl->recv(recv, half_bytes, kNcclUint8, partner, e->comm, s), "ncclRecv");
+      nccl->check(nccl->group_end(), "ncclGroupEnd");
+      launch_half_unpack(recv, buf, nloc, lpos, 1 - a, s);
+    };
+    auto fetch_partner = [&](uint64_t xglob) {  // partner shard's psi -> scratch (NCCL mode)
+      const int partner = e->rank ^ static_cast<int>(xglob >> nloc);
+      nccl->check(nccl->group_start(), "ncclGroupStart");
+      nccl->check(nccl->send(psi, shard_amps * sizeof(double2), kNcclUint8, partner, e->comm, s), "ncclSend");
+      nccl->check(nccl->recv(scratch, shard_amps * sizeof(double2), kNcclUint8, partner, e->comm, s), "ncclRecv");
+      nccl->check(nccl->group_end(), "ncclGroupEnd");
+    };
+
+    int64_t launches = 0, h2d = bl.total, d2h = 0;
     CK(cudaEventRecord(e->ev[0], s));
     CK(cudaMemcpyAsync(db, hb, bl.total, cudaMemcpyHostToDevice, s));
+    // input: shards are consecutive slices of the full index range (identity layout at the start)
+    const size_t first_amp = e->comm ? size_t(e->rank) * shard_amps : 0;
     if (p->input_amps) {
-      CK(cudaMemcpyAsync(psi, p->input_amps, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(psi, p->input_amps + first_amp, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
       h2d += amps * sizeof(double2);
     } else {
       CK(cudaMemsetAsync(psi, 0, amps * sizeof(double2), s));
-      launch_set_basis(psi, static_cast<uint64_t>(p->input_basis), s);
-      launches += 1;
+      const uint64_t idx = static_cast<uint64_t>(p->input_basis);
+      if (idx >= first_amp && idx < first_amp + amps) {
+        launch_set_basis(psi, idx - first_amp, s);
+        launches += 1;
+      }
     }
     CK(cudaEventRecord(e->ev[1], s));
     for (const Launch& l : L.fwd) {
-      if (l.kind == L_REG)
-        launch_pass_reg(1, l.R, l.d, l.grid, l.threads, l.smem, s, psi, nullptr, dsegs, drops, dops, dcoef, part);
-      else
-        launch_fwd(l.d, l.grid, l.smem, s, psi, dops, dcoef);
+      if (l.kind == L_SWAP) {
+        swap_buffer(psi, l.gbit, l.lpos);
+        continue;
+      }
+      for (int sh = 0; sh < nsh; ++sh) {
+        const ShardView v = view(sh);
+        PassDesc d = l.d;
+        d.rank_bits = v.rank_bits;
+        if (l.kind == L_REG)
+          launch_pass_reg(1, l.R, d, l.grid, l.threads, l.smem, s, v.psi, nullptr, dsegs, drops, dops, dcoef, v.part);
+        else
+          launch_fwd(d, l.grid, l.smem, s, v.psi, dops, dcoef);
+        ++launches;
+      }
     }
     CK(cudaEventRecord(e->ev[2], s));
     for (const Launch& l : L.obs) {
-      if (l.d.untiled)
-        launch_obs_direct(l.d, l.grid, s, psi, lam, dterms, part);
-      else
-        launch_obs(l.d, l.grid, l.smem, s, psi, lam, dterms, part);
+      if (l.kind == L_FETCH) {
+        if (e->comm) fetch_partner(l.d.xglob);
+        continue;
+      }
+      for (int sh = 0; sh < nsh; ++sh) {
+        const ShardView v = view(sh);
+        PassDesc d = l.d;
+        d.rank_bits = v.rank_bits;
+        const double2* src = v.psi;
+        if (l.d.xglob) src = e->comm ? scratch : psi + ((uint64_t(sh) ^ (l.d.xglob >> nloc)) << nloc);
+        if (l.kind == L_OBS_DIRECT)
+          launch_obs_direct(d, l.grid, s, v.psi, src, v.lam, dterms, v.part);
+        else
+          launch_obs(d, l.grid, l.smem, s, v.psi, src, v.lam, dterms, v.part);
+        ++launches;
+      }
     }
     CK(cudaEventRecord(e->ev[3], s));
     for (const Launch& l : L.rev) {
-      if (l.kind == L_REG)
-        launch_pass_reg(2, l.R, l.d, l.grid, l.threads, l.smem, s, psi, lam, dsegs, drops, dops, dcoef, part);
-      else
-        launch_rev(l.d, l.grid, l.smem, s, psi, lam, dops, dcoef, part);
+      if (l.kind == L_SWAP) {
+        swap_buffer(psi, l.gbit, l.lpos);
+        swap_buffer(lam, l.gbit, l.lpos);
+        continue;
+      }
+      for (int sh = 0; sh < nsh; ++sh) {
+        const ShardView v = view(sh);
+        PassDesc d = l.d;
+        d.rank_bits = v.rank_bits;
+        if (l.kind == L_REG)
+          launch_pass_reg(2, l.R, d, l.grid, l.threads, l.smem, s, v.psi, v.lam, dsegs, drops, dops, dcoef, v.part);
+        else
+          launch_rev(d, l.grid, l.smem, s, v.psi, v.lam, dops, dcoef, v.part);
+        ++launches;
+      }
     }
     CK(cudaEventRecord(e->ev[4], s));
-    launch_finalize(part, dsums, static_cast<int>(L.sums.size()), dres, s);
+    for (int sh = 0; sh < nsh; ++sh) {
+      launch_finalize(view(sh).part, dsums, static_cast<int>(cnt), dres + sh * cnt, s);
+      ++launches;
+    }
     CK(cudaGetLastError());
-    launches += L.fwd.size() + L.obs.size() + L.rev.size() + 1;
+    // per-shard results -> every rank (NCCL) -> host, summed in shard order (deterministic)
+    int nres = nsh;
+    const double2* dsrc = dres;
+    if (e->comm) {
+      double2* dall = static_cast<double2*>(e->gathered.ptr);
+      nccl->check(nccl->all_gather(dres, dall, cnt * 2, kNcclFloat64, e->comm, s), "ncclAllGather");
+      nres = world;
+      dsrc = dall;
+    }
     double2* hres = static_cast<double2*>(e->hres.ptr);
-    CK(cudaMemcpyAsync(hres, dres, L.sums.size() * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hres, dsrc, cnt * nres * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    d2h += cnt * nres * sizeof(double2);
     CK(cudaEventRecord(e->ev[5], s));
     CK(cudaStreamSynchronize(s));
+    std::vector<double2> tot(cnt, make_double2(0.0, 0.0));
+    for (int r = 0; r < nres; ++r)
+      for (int64_t i = 0; i < cnt; ++i) {
+        tot[i].x += hres[r * cnt + i].x;
+        tot[i].y += hres[r * cnt + i].y;
+      }
 
     const int A = with_reverse ? p->num_derivs : 0;
-    if (energy_out) *energy_out = svg_c128{hres[A].x, hres[A].y};
+    if (energy_out) *energy_out = svg_c128{tot[A].x, tot[A].y};
     if (with_reverse) {
       if (deriv_out)
-        for (int d = 0; d < A; ++d) deriv_out[d] = svg_c128{hres[d].x, hres[d].y};
+        for (int d = 0; d < A; ++d) deriv_out[d] = svg_c128{tot[d].x, tot[d].y};
       if (sums_out) {
         for (int q = 0; q < p->num_params; ++q) sums_out[q] = svg_c128{0.0, 0.0};
         // reference order: gates descending, local parameters ascending (gradients.py:158-165)
@@ -840,8 +1036,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
           for (int j = 0; j < p->gates[i].nderiv; ++j) {
             const int d = first[i] + j;
             svg_c128& dst = sums_out[p->derivs[d].param_ref];
-            dst.re += hres[d].x;
-            dst.im += hres[d].y;
+            dst.re += tot[d].x;
+            dst.im += tot[d].y;
           }
       }
     }
@@ -853,15 +1049,21 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       stats->ms_reverse = elapsed(e->ev[3], e->ev[4]);
       stats->ms_other = stats->ms_total - stats->ms_forward - stats->ms_observable - stats->ms_reverse;
       stats->launches = launches;
-      stats->fwd_passes = static_cast<int32_t>(L.fwd.size());
-      stats->obs_passes = static_cast<int32_t>(L.obs.size());
-      stats->rev_passes = static_cast<int32_t>(L.rev.size());
+      int fp = 0, rp = 0, op = 0;
+      for (const Launch& l : L.fwd) fp += l.kind != L_SWAP;
+      for (const Launch& l : L.rev) rp += l.kind != L_SWAP;
+      for (const Launch& l : L.obs) op += l.kind != L_FETCH;
+      stats->fwd_passes = fp;
+      stats->obs_passes = op;
+      stats->rev_passes = rp;
       stats->tile_qubits = L.k;
       stats->segments = L.reg ? static_cast<int32_t>(L.segs.size()) : 0;
       stats->reg_bits = L.reg ? L.R : 0;
-      stats->pass_bytes = L.pass_bytes;
+      stats->pass_bytes = L.pass_bytes * nsh;
       stats->h2d_bytes = h2d;
       stats->d2h_bytes = d2h;
+      stats->swaps = L.swaps;
+      stats->exchange_bytes = L.swap_bytes;
     }
     return SVG_OK;
   } catch (const InvalidArg& ex) {
@@ -928,10 +1130,66 @@ int svg_engine_create(int device, svg_engine** out) {
   return SVG_OK;
 }
 
+static int log2_shards(int shards) {
+  if (shards < 1 || (shards & (shards - 1))) return -1;
+  return __builtin_ctz(static_cast<unsigned>(shards));
+}
+
+int svg_engine_create_virtual(int device, int shards, svg_engine** out) {
+  const int g = log2_shards(shards);
+  if (g < 0 || g > 6) return fail(SVG_EINVAL, "shards must be a power of two <= 64");
+  const int rc = svg_engine_create(device, out);
+  if (rc != SVG_OK) return rc;
+  (*out)->shard_bits = g;
+  (*out)->shards_local = shards;
+  return SVG_OK;
+}
+
+int svg_nccl_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(SVG_EINVAL, "null id buffer");
+  try {
+    NcclUniqueId id;
+    const Nccl& nc = Nccl::get();
+    nc.check(nc.get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, id.internal, sizeof(id.internal));
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_ENCCL, ex.what());
+  }
+}
+
+int svg_engine_create_sharded(int device, int world, int rank, const uint8_t nccl_id[128], svg_engine** out) {
+  const int g = log2_shards(world);
+  if (g < 0 || g > 6) return fail(SVG_EINVAL, "world size must be a power of two <= 64");
+  if (rank < 0 || rank >= world || !nccl_id) return fail(SVG_EINVAL, "bad rank or null NCCL id");
+  const int rc = svg_engine_create(device, out);
+  if (rc != SVG_OK) return rc;
+  svg_engine* e = *out;
+  e->shard_bits = g;
+  e->shards_local = 1;
+  e->rank = rank;
+  if (world > 1) {
+    try {
+      NcclUniqueId id;
+      std::memcpy(id.internal, nccl_id, sizeof(id.internal));
+      const Nccl& nc = Nccl::get();
+      nc.check(nc.comm_init_rank(&e->comm, world, id, rank), "ncclCommInitRank");
+    } catch (const std::exception& ex) {
+      svg_engine_destroy(e);
+      *out = nullptr;
+      return fail(SVG_ENCCL, ex.what());
+    }
+  }
+  return SVG_OK;
+}
+
 int svg_engine_destroy(svg_engine* e) {
   if (!e) return SVG_OK;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->comm) Nccl::get().comm_destroy(e->comm);
+  e->scratch.release();
+  e->gathered.release();
   e->psi.release();
   e->lam.release();
   e->partials.release();
@@ -985,6 +1243,42 @@ int svg_reverse_sweep(svg_engine* e, const svg_problem* p, svg_c128* sums_out, s
 
 int svg_expectation(svg_engine* e, const svg_problem* p, svg_c128* energy_out, svg_stats* stats) {
   return run(e, p, false, nullptr, nullptr, energy_out, stats);
+}
+
+int svg_plan_schedule(const svg_problem* p, int shards, int tile_qubits, int sms, int32_t* order_out,
+                      int32_t* step_start_out, int32_t* step_swap_out, uint64_t* qmask_out, int32_t* nsteps_out,
+                      int32_t* tile_qubits_out) {
+  try {
+    validate(p);
+    const int g = log2_shards(shards);
+    if (g < 0) throw InvalidArg("shards must be a power of two");
+    const int n = p->num_qubits, nloc = n - g;
+    PlanParams pp;
+    pp.n = nloc;
+    pp.k = choose_tile_qubits(nloc, tile_qubits, sms > 0 ? sms : 148);
+    pp.b = (nloc <= pp.k) ? nloc : std::min(5, pp.k - 2);
+    std::vector<GateShape> shapes(p->num_gates);
+    for (int i = 0; i < p->num_gates; ++i) shapes[i] = gate_shape(p->gates[i]);
+    const std::vector<Step> steps = plan_schedule(shapes, n, g, pp, nullptr);
+    int pos = 0;
+    for (size_t j = 0; j < steps.size(); ++j) {
+      if (step_start_out) step_start_out[j] = pos;
+      // swap steps: (gbit << 8 | lpos) + 1; pass steps: 0
+      if (step_swap_out) step_swap_out[j] = steps[j].swap ? ((steps[j].gbit << 8) | steps[j].lpos) + 1 : 0;
+      if (qmask_out) qmask_out[j] = steps[j].swap ? 0 : steps[j].pass.qmask;
+      if (!steps[j].swap)
+        for (int gi : steps[j].pass.items) {
+          if (order_out) order_out[pos] = gi;
+          ++pos;
+        }
+    }
+    if (step_start_out) step_start_out[steps.size()] = pos;
+    if (nsteps_out) *nsteps_out = static_cast<int32_t>(steps.size());
+    if (tile_qubits_out) *tile_qubits_out = pp.k;
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_EINVAL, ex.what());
+  }
 }
 
 int svg_plan_inspect(const svg_problem* p, int tile_qubits, int sms, int32_t* order_out,

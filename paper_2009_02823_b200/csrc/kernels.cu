@@ -16,6 +16,8 @@
 // rerun is bit-identical.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "device.cuh"
 #include "kernels.h"
 #include "tile_ops.cuh"
@@ -36,12 +38,13 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pass(double2* __restrict__ psi
   const uint64_t ntiles = 1ull << (d.n - d.k);
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
+    const uint64_t sbase = base | d.rank_bits;  // physical index bits for Z-signs / controls
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) tile[t] = psi[gidx(base, t, hi, d.b)];
     __syncthreads();
     for (int o = d.op_begin; o < d.op_end; ++o) {
       const DevOp op = ops[o];
-      if ((base & op.co) != op.co) continue;
-      tile_apply(tile, d.k, op, coef + op.coef, base);
+      if ((sbase & op.co) != op.co) continue;
+      tile_apply(tile, d.k, op, coef + op.coef, sbase);
       __syncthreads();
     }
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) psi[gidx(base, t, hi, d.b)] = tile[t];
@@ -50,11 +53,15 @@ __global__ void __launch_bounds__(kThreads) k_fwd_pass(double2* __restrict__ psi
 }
 
 __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict__ psi,
+                                                       const double2* __restrict__ src_state,
                                                        double2* __restrict__ lam, PassDesc d,
                                                        const DevTerm* __restrict__ terms,
                                                        double2* __restrict__ partials) {
+  // src_state: the shard whose amplitudes feed this pass's terms (== psi unless the
+  // terms flip rank bits, d.xglob != 0: then the partner shard, fetched or peer-mapped)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << d.k;
+  const bool remote = d.xglob != 0;
   double2* tile = reinterpret_cast<double2*>(smem_raw);
   double2* wsum = tile + N;
   uint64_t* hi = reinterpret_cast<uint64_t*>(wsum + kWarps);
@@ -64,14 +71,16 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
   const uint64_t ntiles = 1ull << (d.n - d.k);
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
-    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) tile[t] = psi[gidx(base, t, hi, d.b)];
+    const uint64_t sbase = base | d.rank_bits;  // physical index bits for Z-signs / controls
+    const uint64_t src_bits = sbase ^ d.xglob;  // non-tile bits of the source amplitude index
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) tile[t] = src_state[gidx(base, t, hi, d.b)];
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
       double2 acc = make_double2(0.0, 0.0);
       for (int j = d.op_begin; j < d.op_end; ++j) {
         const DevTerm tm = terms[j];
         const uint32_t src = t ^ tm.xl;
-        const int sg = par32(src & tm.zl) ^ par64(base & tm.zo);
+        const int sg = par32(src & tm.zl) ^ par64(src_bits & tm.zo);
         acc = cfma(cneg_if(tm.c, sg), tile[src], acc);
       }
       const uint64_t m = gidx(base, t, hi, d.b);
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
       } else {
         lam[m] = acc;
       }
-      e = cjfma(tile[t], acc, e);
+      e = cjfma(remote ? psi[m] : tile[t], acc, e);
     }
     __syncthreads();
   }
@@ -97,19 +106,21 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
 
 // Untiled observable pass for flip masks too wide for a tile: plain gathers.
 __global__ void __launch_bounds__(kThreads) k_obs_direct(const double2* __restrict__ psi,
+                                                         const double2* __restrict__ src_state,
                                                          double2* __restrict__ lam, PassDesc d,
                                                          const DevTerm* __restrict__ terms,
                                                          double2* __restrict__ partials) {
   __shared__ double2 wsum[kWarps];
   double2 e = make_double2(0.0, 0.0);
   const uint64_t dim = 1ull << d.n;
+  const uint64_t src_bits = d.rank_bits ^ d.xglob;  // rank bits of the source amplitude index
   for (uint64_t m = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; m < dim; m += uint64_t(gridDim.x) * blockDim.x) {
     double2 acc = make_double2(0.0, 0.0);
     for (int j = d.op_begin; j < d.op_end; ++j) {
       const DevTerm tm = terms[j];
-      const uint64_t x = uint64_t(tm.xl) | (uint64_t(tm.zl) << 32);
+      const uint64_t x = uint64_t(tm.xl) | (uint64_t(tm.zl) << 32);  // local part of the flip mask
       const uint64_t src = m ^ x;
-      acc = cfma(cneg_if(tm.c, par64(src & tm.zo)), psi[src], acc);
+      acc = cfma(cneg_if(tm.c, par64((src | src_bits) & tm.zo)), src_state[src], acc);
     }
     if (d.accumulate) {
       const double2 old = lam[m];
@@ -147,6 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_rev_pass(double2* __restrict__ phi
   const uint64_t ntiles = 1ull << (d.n - d.k);
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
+    const uint64_t sbase = base | d.rank_bits;  // physical index bits for Z-signs / controls
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
       const uint64_t m = gidx(base, t, hi, d.b);
       tp[t] = phi[m];
@@ -155,11 +167,11 @@ __global__ void __launch_bounds__(kThreads) k_rev_pass(double2* __restrict__ phi
     __syncthreads();
     for (int o = d.op_begin; o < d.op_end; ++o) {
       const DevOp op = ops[o];
-      if ((base & op.co) != op.co) continue;
+      if ((sbase & op.co) != op.co) continue;
       if (op.kind <= OP_APPLY_MAT2) {
-        tile_apply(op.buf ? tl : tp, d.k, op, coef + op.coef, base);
+        tile_apply(op.buf ? tl : tp, d.k, op, coef + op.coef, sbase);
       } else {
-        const double2 v = warp_sum(tile_ip(tp, tl, d.k, op, coef + op.coef, base));
+        const double2 v = warp_sum(tile_ip(tp, tl, d.k, op, coef + op.coef, sbase));
         if (lane == 0) {
           double2& a = wacc[warp * d.nslots + op.slot];
           a = make_double2(a.x + v.x, a.y + v.y);
@@ -199,6 +211,39 @@ __global__ void k_finalize(const double2* __restrict__ partials, const SumSpec* 
 
 __global__ void k_set_basis(double2* psi, uint64_t idx) { psi[idx] = make_double2(1.0, 0.0); }
 
+// Qubit swap between rank bit `gbit` and local bit `lpos` (virtual shards in one
+// allocation).  Amplitude (rank r, local m) with r_g = a, m_p = c moves to
+// (r with r_g = c, m with m_p = a): shard pairs exchange lower[m | p] <-> upper[m].
+__global__ void k_swap_virtual(double2* __restrict__ state, int nloc, int nshards, int gbit, int lpos) {
+  const uint64_t half = 1ull << (nloc - 1);
+  const uint64_t pairs = uint64_t(nshards / 2) * half;
+  const uint64_t pbit = 1ull << lpos;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < pairs; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t pr = i >> (nloc - 1), m0 = i & (half - 1);
+    const uint64_t lo_rank = ((pr >> gbit) << (gbit + 1)) | (pr & ((1ull << gbit) - 1));  // rank bit gbit = 0
+    const uint64_t hi_rank = lo_rank | (1ull << gbit);
+    const uint64_t m = ((m0 >> lpos) << (lpos + 1)) | (m0 & (pbit - 1));  // local bit lpos = 0
+    double2* a = state + (lo_rank << nloc) + (m | pbit);
+    double2* b = state + (hi_rank << nloc) + m;
+    const double2 t = *a;
+    *a = *b;
+    *b = t;
+  }
+}
+
+// packed[i] = shard[i with bit lpos inserted = val]   (and the inverse scatter)
+__global__ void k_half_pack(const double2* __restrict__ shard, double2* __restrict__ packed, int nloc, int lpos,
+                            int val, int unpack) {
+  const uint64_t half = 1ull << (nloc - 1);
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < half; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t m = ((i >> lpos) << (lpos + 1)) | (i & ((1ull << lpos) - 1)) | (uint64_t(val) << lpos);
+    if (unpack)
+      const_cast<double2*>(shard)[m] = packed[i];
+    else
+      packed[i] = shard[m];
+  }
+}
+
 // ------------------------------------------------------------ launchers --
 
 size_t fwd_smem(int k, int b) { return (sizeof(double2) << k) + (sizeof(uint64_t) << (k - b)); }
@@ -233,13 +278,13 @@ void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double
                 const DevOp* ops, const double2* coef) {
   k_fwd_pass<<<grid, kThreads, smem, s>>>(psi, d, ops, coef);
 }
-void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi,
+void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi, const double2* src,
                 double2* lam, const DevTerm* terms, double2* partials) {
-  k_obs_pass<<<grid, kThreads, smem, s>>>(psi, lam, d, terms, partials);
+  k_obs_pass<<<grid, kThreads, smem, s>>>(psi, src, lam, d, terms, partials);
 }
-void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, double2* lam,
-                       const DevTerm* terms, double2* partials) {
-  k_obs_direct<<<grid, kThreads, 0, s>>>(psi, lam, d, terms, partials);
+void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, const double2* src,
+                       double2* lam, const DevTerm* terms, double2* partials) {
+  k_obs_direct<<<grid, kThreads, 0, s>>>(psi, src, lam, d, terms, partials);
 }
 void launch_rev(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* phi, double2* lam,
                 const DevOp* ops, const double2* coef, double2* partials) {
@@ -251,5 +296,19 @@ void launch_finalize(const double2* partials, const SumSpec* specs, int count, d
   k_finalize<<<(count + 127) / 128, 128, 0, s>>>(partials, specs, count, out);
 }
 void launch_set_basis(double2* psi, uint64_t idx, cudaStream_t s) { k_set_basis<<<1, 1, 0, s>>>(psi, idx); }
+
+static int stream_grid(uint64_t items) {
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((items + 255) / 256, 148ull * 16)));
+}
+void launch_swap_virtual(double2* state, int nloc, int nshards, int gbit, int lpos, cudaStream_t s) {
+  const uint64_t pairs = uint64_t(nshards / 2) << (nloc - 1);
+  k_swap_virtual<<<stream_grid(pairs), 256, 0, s>>>(state, nloc, nshards, gbit, lpos);
+}
+void launch_half_pack(const double2* shard, double2* packed, int nloc, int lpos, int val, cudaStream_t s) {
+  k_half_pack<<<stream_grid(1ull << (nloc - 1)), 256, 0, s>>>(shard, packed, nloc, lpos, val, 0);
+}
+void launch_half_unpack(const double2* packed, double2* shard, int nloc, int lpos, int val, cudaStream_t s) {
+  k_half_pack<<<stream_grid(1ull << (nloc - 1)), 256, 0, s>>>(shard, const_cast<double2*>(packed), nloc, lpos, val, 1);
+}
 
 }  // namespace svgb

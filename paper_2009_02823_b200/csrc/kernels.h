@@ -16,10 +16,17 @@ int occupancy(int which /*0 fwd, 1 obs, 2 rev*/, size_t smem);
 
 void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* psi,
                 const DevOp* ops, const double2* coef);
-void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi,
+void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi, const double2* src,
                 double2* lam, const DevTerm* terms, double2* partials);
-void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, double2* lam,
-                       const DevTerm* terms, double2* partials);
+void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, const double2* src,
+                       double2* lam, const DevTerm* terms, double2* partials);
+// qubit swap of a sharded state (virtual shards in one allocation): for every
+// shard pair differing in rank bit `gbit`, exchange lower's amplitudes with
+// local bit `lpos` = 1 and upper's with local bit `lpos` = 0.
+void launch_swap_virtual(double2* state, int nloc, int nshards, int gbit, int lpos, cudaStream_t s);
+// gather / scatter the half of a shard whose local bit `lpos` equals `val` (NCCL exchange staging)
+void launch_half_pack(const double2* shard, double2* packed, int nloc, int lpos, int val, cudaStream_t s);
+void launch_half_unpack(const double2* packed, double2* shard, int nloc, int lpos, int val, cudaStream_t s);
 void launch_rev(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* phi, double2* lam,
                 const DevOp* ops, const double2* coef, double2* partials);
 void launch_finalize(const double2* partials, const SumSpec* specs, int count, double2* out,

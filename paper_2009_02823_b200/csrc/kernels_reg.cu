@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   const uint64_t ntiles = 1ull << (d.n - d.k);
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
+    const uint64_t sbase = base | d.rank_bits;  // physical index bits for Z-signs / controls
     const uint64_t next = T + gridDim.x;
     Map<R> m;
     make_map<R>(m, segs[d.seg_begin], sq, warp, wbits);
@@ -416,8 +417,8 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
         }
         for (int o = sg.op_begin - d.op_begin; o < sg.op_end - d.op_begin; ++o) {
           const RegOp& op = sops[o];
-          if ((base & op.co) != op.co) continue;
-          const uint32_t slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(base & op.zo)) & 1u;
+          if ((sbase & op.co) != op.co) continue;
+          const uint32_t slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(sbase & op.zo)) & 1u;
           OpCtx c;
           c.a = op.a;
           c.bb = slw ? -op.bb : op.bb;  // uniform part of the partner sign
@@ -460,11 +461,11 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
         }
         for (int o = sg.op_begin; o < sg.op_end; ++o) {
           const DevOp op = ops[o];
-          if ((base & op.co) != op.co) continue;
+          if ((sbase & op.co) != op.co) continue;
           if (op.kind <= OP_APPLY_MAT2) {
-            tile_apply(op.buf ? st1 : st0, d.k, op, coef + op.coef, base);
+            tile_apply(op.buf ? st1 : st0, d.k, op, coef + op.coef, sbase);
           } else {
-            const double2 val = warp_sum(tile_ip(st0, st1, d.k, op, coef + op.coef, base));
+            const double2 val = warp_sum(tile_ip(st0, st1, d.k, op, coef + op.coef, sbase));
             if (lane == 0) {
               double2& acc = wacc[warp * d.nslots + op.slot];
               acc = make_double2(acc.x + val.x, acc.y + val.y);

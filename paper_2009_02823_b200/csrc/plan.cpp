@@ -25,44 +25,125 @@ static uint64_t pad_tile(uint64_t q, int n, int k) {
   return q;
 }
 
-std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp) {
+Pass plan_one_pass(const std::vector<GateShape>& shapes, std::vector<char>& done, const PlanParams& pp,
+                   uint64_t forbidden_flip) {
   const int G = static_cast<int>(shapes.size());
-  const uint64_t full = low_mask(pp.n);
-  std::vector<char> done(G, 0);
-  std::vector<Pass> passes;
-  int first = 0;
-  int remaining = G;
-  while (remaining > 0) {
-    while (done[first]) ++first;
-    Pass p;
-    uint64_t q = low_mask(pp.b);
-    uint64_t flip_blocked = 0, diag_blocked = 0;
-    int derivs = 0;
-    for (int i = first; i < G; ++i) {
-      if (done[i]) continue;
-      const GateShape& s = shapes[i];
-      const uint64_t diag = s.touch & ~s.flip;
-      bool ok = !(s.touch & flip_blocked) && !(s.flip & diag_blocked);
-      ok = ok && popc(q | s.flip) <= pp.k;
-      ok = ok && static_cast<int>(p.items.size()) < pp.max_items;
-      ok = ok && derivs + s.nderiv <= pp.max_derivs;
-      if (ok) {
-        q |= s.flip;
-        p.items.push_back(i);
-        derivs += s.nderiv;
-        done[i] = 1;
-        --remaining;
-      } else {
-        flip_blocked |= s.flip;
-        diag_blocked |= diag;
-        if ((flip_blocked & full) == full) break;  // nothing later can commute forward
-      }
+  // every qubit counts for the early exit, including global (rank) positions
+  uint64_t all = 0;
+  for (const GateShape& s : shapes) all |= s.touch;
+  Pass p;
+  uint64_t q = low_mask(pp.b);
+  uint64_t flip_blocked = 0, diag_blocked = 0;
+  int derivs = 0;
+  for (int i = 0; i < G; ++i) {
+    if (done[i]) continue;
+    const GateShape& s = shapes[i];
+    const uint64_t diag = s.touch & ~s.flip;
+    bool ok = !(s.touch & flip_blocked) && !(s.flip & diag_blocked) && !(s.flip & forbidden_flip);
+    ok = ok && popc(q | s.flip) <= pp.k;
+    ok = ok && static_cast<int>(p.items.size()) < pp.max_items;
+    ok = ok && derivs + s.nderiv <= pp.max_derivs;
+    if (ok) {
+      q |= s.flip;
+      p.items.push_back(i);
+      derivs += s.nderiv;
+      done[i] = 1;
+    } else {
+      flip_blocked |= s.flip;
+      diag_blocked |= diag;
+      if ((flip_blocked & all) == all) break;  // nothing later can commute forward
     }
+  }
+  p.qmask = pad_tile(q, pp.n, pp.k);
+  return p;
+}
+
+std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp) {
+  std::vector<char> done(shapes.size(), 0);
+  std::vector<Pass> passes;
+  size_t placed = 0;
+  while (placed < shapes.size()) {
+    Pass p = plan_one_pass(shapes, done, pp, 0);
     if (p.items.empty()) throw std::runtime_error("planner made no progress (gate flip set wider than tile)");
-    p.qmask = pad_tile(q, pp.n, pp.k);
+    placed += p.items.size();
     passes.push_back(std::move(p));
   }
   return passes;
+}
+
+uint64_t remap_mask(uint64_t m, const std::vector<int>& l2p) {
+  uint64_t r = 0;
+  for (uint64_t v = m; v; v &= v - 1) r |= 1ull << l2p[__builtin_ctzll(v)];
+  return r;
+}
+
+std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, int g, const PlanParams& pp,
+                                std::vector<int>* l2p_final) {
+  const int nloc = n - g;
+  if (pp.n != nloc) throw std::runtime_error("plan_schedule: PlanParams.n must be the local qubit count");
+  const int G = static_cast<int>(logical.size());
+  std::vector<int> l2p(n), p2l(n);
+  for (int q = 0; q < n; ++q) l2p[q] = p2l[q] = q;
+  const uint64_t rank_mask = g ? (low_mask(n) & ~low_mask(nloc)) : 0;
+  std::vector<GateShape> phys(G);
+  auto refresh = [&]() {
+    for (int i = 0; i < G; ++i) {
+      phys[i] = logical[i];
+      phys[i].flip = remap_mask(logical[i].flip, l2p);
+      phys[i].touch = remap_mask(logical[i].touch, l2p);
+    }
+  };
+  refresh();
+  std::vector<char> done(G, 0);
+  std::vector<Step> steps;
+  int placed = 0, swaps_in_a_row = 0;
+  while (placed < G) {
+    std::vector<char> trial = done;
+    Pass p = plan_one_pass(phys, trial, pp, rank_mask);
+    if (!p.items.empty()) {
+      done.swap(trial);
+      placed += static_cast<int>(p.items.size());
+      Step st;
+      st.pass = std::move(p);
+      st.l2p = l2p;
+      steps.push_back(std::move(st));
+      swaps_in_a_row = 0;
+      continue;
+    }
+    // the earliest pending gate flips a rank bit: swap it into a local position
+    int gi = 0;
+    while (done[gi]) ++gi;
+    const uint64_t need = phys[gi].flip & rank_mask;
+    if (!need || ++swaps_in_a_row > 2 * g + 2) throw std::runtime_error("sharded planner made no progress");
+    const int pg = __builtin_ctzll(need);
+    int best = -1, best_next = -1;
+    for (int lp = nloc - 1; lp >= 0; --lp) {  // any local position; ties prefer high ones (contiguous halves)
+      if ((phys[gi].flip >> lp) & 1) continue;
+      int next = G;  // index of the next pending gate flipping this position
+      for (int i = gi; i < G; ++i)
+        if (!done[i] && ((phys[i].flip >> lp) & 1)) {
+          next = i;
+          break;
+        }
+      if (next > best_next) {
+        best_next = next;
+        best = lp;
+      }
+    }
+    if (best < 0) throw std::runtime_error("no local qubit available to swap with a rank bit");
+    Step st;
+    st.swap = true;
+    st.gbit = pg - nloc;
+    st.lpos = best;
+    st.l2p = l2p;
+    steps.push_back(std::move(st));
+    std::swap(p2l[pg], p2l[best]);
+    l2p[p2l[pg]] = pg;
+    l2p[p2l[best]] = best;
+    refresh();
+  }
+  if (l2p_final) *l2p_final = l2p;
+  return steps;
 }
 
 std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp,

@@ -48,6 +48,12 @@ GateShape gate_shape(const svg_gate& g);
 // Forward gate passes; the reverse sweep walks the same passes backwards.
 std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp);
 
+// One greedy pass over the not-yet-`done` gates (marks the gates it takes).
+// Gates flipping a `forbidden_flip` position (a sharded qubit) are skipped and
+// block their qubits like any other excluded gate.
+Pass plan_one_pass(const std::vector<GateShape>& shapes, std::vector<char>& done, const PlanParams& pp,
+                   uint64_t forbidden_flip);
+
 // Observable passes: terms grouped so each pass's flip masks fit one tile.
 // Terms whose flip mask cannot share a tile with the low qubits go to `direct`
 // (handled by an untiled gather kernel).
@@ -67,6 +73,28 @@ struct Segment {
 // each segment takes the register set that unlocks the most pending gates.
 std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
                                    const std::vector<char>& dense, int k, int regbits);
+
+// ---- sharded schedules (state split over 2^g ranks by its top g PHYSICAL qubits) ----
+//
+// The schedule tracks a logical -> physical qubit map.  Gates only flip local
+// physical positions; when the next gates need a flip on a rank bit, a SWAP
+// step exchanges that rank bit with a local position (a pairwise half-shard
+// exchange between ranks r and r ^ 2^gbit), chosen as the local qubit whose
+// next flip lies furthest ahead.  Diagonal factors and controls on rank bits
+// never need a swap (the rank bits enter the kernels' sign/control tests).
+struct Step {
+  bool swap = false;
+  int gbit = 0, lpos = 0;   // swap: rank bit gbit <-> local physical position lpos
+  Pass pass;                // pass: items = gate indices, qmask over physical local positions
+  std::vector<int> l2p;     // logical -> physical map in effect for this step's gates
+};
+
+uint64_t remap_mask(uint64_t m, const std::vector<int>& l2p);
+
+// n total qubits, g rank bits (pp.n must be n - g); returns the forward schedule
+// and the final map (the observable and the reverse sweep start from it).
+std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, int g, const PlanParams& pp,
+                                std::vector<int>* l2p_final);
 
 // Tile size choice for n qubits on `sms` SMs (auto when requested == 0).
 int choose_tile_qubits(int n, int requested, int sms);
