@@ -20,6 +20,7 @@ from .adjoint import (
     reverse_mode_gradient,
     sweep,
 )
+from . import distributed
 from .configs import Workload, build_workload
 from .ir import (
     Circuit,

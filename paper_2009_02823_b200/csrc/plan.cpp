@@ -130,7 +130,7 @@ std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, in
         best = lp;
       }
     }
-    if (best < 0) throw std::runtime_error("no local qubit available to swap with a rank bit");
+    if (best < 0) throw std::runtime_error("a gate flips more qubits than a shard holds locally (use fewer shards)");
     Step st;
     st.swap = true;
     st.gbit = pg - nloc;

@@ -1,0 +1,142 @@
+"""GPU parity of the sharded engine (SURVEY.md §8 row e) on one device.
+
+A virtual engine holds 2/4/8 shards of the state on one GPU and runs exactly
+the distributed schedule of an NCCL job (top qubits = shard bits, rank-bit <->
+local-qubit swaps, partner-shard fetches for observable terms that flip shard
+bits, per-shard partial sums combined in shard order); only the exchange
+transport differs (device copies instead of ncclSend/Recv).  Results must
+meet the same bar as the single-shard engine against the reference's golden
+outputs and the oracle.
+"""
+import numpy as np
+import pytest
+
+import paper_2009_02823_b200 as sv
+from cases import config_cases, small_cases
+from conftest import cvec, load_golden, materialize, max_err
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = 1e-10
+ENERGY_TOL = 1e-12
+
+GOLD = load_golden()
+SMALL = {**small_cases(), **config_cases()}
+_ENGINES: dict = {}
+
+
+def _engine(shards):
+    e = _ENGINES.get(shards)
+    if e is None:
+        e = _ENGINES[shards] = sv.distributed.virtual_engine(shards)
+    return e
+
+
+def _run(circ, theta, obs, inp, method, eng, stats=None):
+    if method == "non_hermitian":
+        return sv.non_hermitian_gradient(circ, theta, obs, inp, engine=eng)
+    return sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng, stats=stats)
+
+
+def _cases():
+    out = []
+    for name in sorted(SMALL):
+        circ, _, _, _, _ = materialize(SMALL[name])
+        for shards in (2, 4, 8):
+            if circ.num_qubits - (shards.bit_length() - 1) >= 2:  # 2-qubit gates need 2 local qubits
+                out.append((name, shards))
+    return out
+
+
+@pytest.mark.parametrize("name,shards", _cases())
+def test_virtual_shards_match_reference_golden(name, shards):
+    rec = GOLD[name]
+    circ, theta, obs, inp, method = materialize(SMALL[name])
+    rep = _run(circ, theta, obs, inp, method, _engine(shards))
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+    assert vars(rep.counters) == rec["counters"]
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("name", ["cfg5_n15", "cfg4_n16", "cfg3_n14", "cfg2_n12"])
+def test_virtual_shards_both_kernel_families(name, kernel, shards):
+    """Tiles narrower than the shard (register and shared-memory kernels) with swaps."""
+    rec = GOLD[name]
+    circ, theta, obs, inp, _ = materialize(SMALL[name])
+    eng = _engine(shards)
+    eng.set_option("kernel", kernel)
+    stats = {}
+    try:
+        rep = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng, stats=stats)
+    finally:
+        eng.set_option("kernel", 0)
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+    assert stats["swaps"] > 0 and stats["exchange_bytes"] > 0
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+@pytest.mark.parametrize("method", ["reverse", "non_hermitian"])
+def test_virtual_shards_every_gate_kind(shards, method):
+    """Dense and controlled gates, complex generators and global-flip observable terms."""
+    from cases import all_kinds_circuit, mixed_observable, random_amplitudes
+    from oracle import oracle
+
+    n = 12
+    circ = all_kinds_circuit(sv, n)
+    theta = np.random.default_rng([7, n]).uniform(-np.pi, 2 * np.pi, circ.num_params)
+    complex_obs = method == "non_hermitian"
+    obs = mixed_observable(sv, n, 33, count=12, letters="XYZ+-" if complex_obs else "XYZH", complex_coeffs=complex_obs)
+    inp = sv.StateVector(n, random_amplitudes(n, 4))
+    eng = _engine(shards)
+    for tile in (0, 8, 9):
+        eng.set_option("tile_qubits", tile)
+        try:
+            rep = _run(circ, theta, obs, inp, method, eng)
+        finally:
+            eng.set_option("tile_qubits", 0)
+        if complex_obs:
+            vals, energy, _ = oracle.non_hermitian_values(circ, theta, obs, inp.amplitudes)
+        else:
+            vals, energy, _ = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+        assert max_err(rep.values, vals) <= GRAD_TOL, tile
+        assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("shards", [2, 8])
+def test_virtual_shards_wide_flip_terms(shards):
+    """hadamard_all: Pauli strings flipping every qubit, shard bits included (partner fetch)."""
+    from oracle import oracle
+
+    n = 13
+    circ = sv.Circuit(n, tuple(sv.ry(q, q) for q in range(n)) + tuple(sv.cx(q, (q + 1) % n) for q in range(n)), n)
+    theta = np.linspace(0.1, 2.9, n)
+    obs = sv.builtin_observable("hadamard_all", n)
+    inp = sv.init_basis_state(n)
+    rep = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=_engine(shards))
+    vals, energy, _ = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 22), (4, 22), (5, 21)])
+@pytest.mark.parametrize("shards", [2, 8])
+def test_virtual_shards_match_single_shard_midsize(cfg, n, shards):
+    w = sv.build_workload(cfg, n)
+    inp = sv.BasisState(n)
+    ref = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp)
+    rep = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp, engine=_engine(shards))
+    assert max_err(rep.values, ref.values) <= GRAD_TOL
+    assert abs(rep.energy - ref.energy) <= ENERGY_TOL
+
+
+def test_virtual_shards_expectation_and_determinism():
+    circ, theta, obs, inp, _ = materialize(SMALL["cfg5_n15"])
+    eng = _engine(4)
+    e = sv.circuit_expectation(circ, theta, obs, inp, engine=eng)
+    assert abs(e - complex(*GOLD["cfg5_n15"]["energy"])) <= ENERGY_TOL
+    a = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng)
+    b = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng)
+    assert np.array_equal(a.values, b.values) and a.energy == b.energy
