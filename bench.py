@@ -20,9 +20,16 @@ passes, finalize) of the configured circuit.  Rank 0 prints ONE JSON line.
   (oracle/, "port") on the host cores, bounded sample (rank 0, N=1).
 * ``--impl reference``: that same CPU port as the reference arm.
 
-Multi-GPU (torchrun, N>1): replicas -- each rank evaluates the full gradient
-independently (state sharding is not wired into the bench yet); value sums
-all ranks' gradients over the max-over-ranks time.
+Multi-GPU (torchrun, N>1), max-over-ranks device time:
+* configs BASELINE.json runs on one GPU (cfg 1-3; the default cfg 2 is
+  "Single GPU"): replicas -- each rank evaluates full gradients of its own
+  copy (no data-path collective), ``scaling: "weak"``, value = all ranks'
+  gradients / time;
+* the sharded configs (cfg 4 "strong-scaling ... sharded on its top qubits",
+  cfg 5) or ``--shard``: ONE state split over the N ranks by its top log2(N)
+  qubits (paper_2009_02823_b200.distributed.nccl_engine: NCCL half-shard
+  exchanges for qubit swaps, partner fetches, one all-gather of partial
+  sums), ``scaling: "strong"``, value = gradients of the whole job / time.
 """
 from __future__ import annotations
 
@@ -55,6 +62,7 @@ def _args():
     ap.add_argument("--reg-bits", type=int, default=0, help="reverse register tile: 2^bits amplitudes/thread (3/4)")
     ap.add_argument("--reg-bits-fwd", type=int, default=0, help="forward register tile: 2^bits amplitudes/thread")
     ap.add_argument("--prefetch", action="store_true", help="stream tiles with cp.async.bulk into shared memory")
+    ap.add_argument("--shard", action="store_true", help="N>1: shard one state over the ranks (default for cfg 4/5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -194,7 +202,14 @@ def run_ours(args, rank, world, local_rank):
     w = sv.build_workload(args.config, args.qubits)
     n = w.num_qubits
     S = 16 << n
-    eng = _native.engine(local_rank)
+    sharded = world > 1 and (args.shard or args.config in (4, 5))
+    if sharded:
+        eng = sv.distributed.nccl_engine(local_rank)
+        jobs = 1  # the N ranks compute one gradient together
+    else:
+        eng = _native.engine(local_rank)
+        jobs = world  # independent replicas
+    S_rank = S // world if sharded else S
     eng.set_option("tile_qubits", args.tile_qubits)
     if args.reg_bits:
         eng.set_option("reg_bits", args.reg_bits)
@@ -207,7 +222,7 @@ def run_ours(args, rank, world, local_rank):
     basis = sv.BasisState(n)
 
     def step(inp, st):
-        return sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp, stats=st)
+        return sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp, stats=st, engine=eng)
 
     for _ in range(args.warmup):
         step(basis, {})
@@ -244,7 +259,9 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not (sharded and S > (4 << 30)):
+        # (sharded n >= 29: the API's full-size host StateVector on every rank would
+        # need N x S of pinned host memory; e2e is reported for the unsharded runs)
         pinned = torch.empty(1 << n, dtype=torch.complex128, pin_memory=True)
         host = pinned.numpy()
         host[:] = 0
@@ -261,21 +278,21 @@ def run_ours(args, rank, world, local_rank):
             t0 = time.perf_counter()
             rep = step(state, st)
             wall += time.perf_counter() - t0
-        e2e = {"value": world * args.steps / wall, "unit": UNIT,
+        e2e = {"value": jobs * args.steps / wall, "unit": UNIT,
                "h2d_bytes_per_step": int(st["h2d_bytes"]), "d2h_bytes_per_step": int(st["d2h_bytes"])}
         if dist:
             t = torch.tensor([wall], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e["value"] = world * args.steps / float(t.item())
+            e2e["value"] = jobs * args.steps / float(t.item())
         assert np.array_equal(rep.values, last.values)
 
     if rank != 0:
         return
     peak, peak_src = _peak()
     avg_launch_ms = rev_ms / max(1, rev_launches)
-    achieved = 4 * S / (avg_launch_ms * 1e-3) / 1e9
+    achieved = 4 * S_rank / (avg_launch_ms * 1e-3) / 1e9
     traffic = _traffic_per_launch()
-    value = world * args.steps / (total_ms * 1e-3)
+    value = jobs * args.steps / (total_ms * 1e-3)
     B_alg = 6 * w.num_gates * S  # gate-level algorithmic bytes per gradient
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -285,17 +302,19 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (BASELINE cfg{args.config} generator, seed 0, |0..0> input; random-init theta)",
         "config": {
             "workload": f"cfg{args.config}", "num_qubits": n, "num_gates": w.num_gates,
             "num_params": w.circuit.num_params, "num_terms": len(w.observable.terms),
             "state_bytes": S, "l2": "flushed between timed steps (256 MiB write, outside the events)",
-            "parallelism": "replicas" if world > 1 else "single-gpu", "tile_qubits": tile_k,
+            "parallelism": (f"state sharded over {world} ranks (top {world.bit_length() - 1} qubits)" if sharded
+                            else "replicas" if world > 1 else "single-gpu"), "tile_qubits": tile_k,
+            "swaps_per_gradient": int(st_last["swaps"]), "exchange_bytes_per_rank": int(st_last["exchange_bytes"]),
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "k_rev_pass", "bytes_per_launch": 4 * S,
+            "traffic": traffic, "kernel": "k_rev_pass", "bytes_per_launch": 4 * S_rank,
             "avg_launch_ms": avg_launch_ms, "peak_source": peak_src,
         },
         "phase_ms": {k: round(v, 4) for k, v in phases.items()},

@@ -155,6 +155,9 @@ struct svg_engine {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4, opt_prefetch = 0;
+  // virtual engines: run the NCCL-mode data path (half-shard pack -> copy ->
+  // unpack, partner fetch into scratch) with device copies as the transport
+  int64_t opt_emulate_transport = 0;
   DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
   // sharding: the state is split over 2^shard_bits shards by its top physical
@@ -866,6 +869,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     e->hblob.reserve(bl.total);
     e->results.reserve(cnt * std::max(nsh, world) * sizeof(double2));
     e->hres.reserve(cnt * std::max(nsh, world) * sizeof(double2));
+    const bool emulate = !e->comm && nsh > 1 && e->opt_emulate_transport;
+    if (emulate) e->scratch.reserve(2 * shard_amps * sizeof(double2));
     if (e->comm) {
       e->scratch.reserve(shard_amps * sizeof(double2));
       e->gathered.reserve(cnt * world * sizeof(double2));
@@ -903,6 +908,19 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     const size_t half_bytes = shard_amps / 2 * sizeof(double2);
     // rank bit `gbit` <-> local position `lpos` for one state buffer (see plan.h)
     auto swap_buffer = [&](double2* buf, int gbit, int lpos) {
+      if (emulate) {  // every pair runs the rank-side pack / exchange / unpack sequence
+        for (int r = 0; r < nsh; ++r) {
+          if ((r >> gbit) & 1) continue;
+          const int q = r | (1 << gbit);
+          double2* sr = scratch;                  // r's outgoing half
+          double2* sq = scratch + shard_amps / 2; // q's outgoing half
+          launch_half_pack(buf + r * shard_amps, sr, nloc, lpos, 1, s);
+          launch_half_pack(buf + q * shard_amps, sq, nloc, lpos, 0, s);
+          launch_half_unpack(sq, buf + r * shard_amps, nloc, lpos, 1, s);
+          launch_half_unpack(sr, buf + q * shard_amps, nloc, lpos, 0, s);
+        }
+        return;
+      }
       if (!e->comm) {
         launch_swap_virtual(buf, nloc, nsh, gbit, lpos, s);
         return;
@@ -970,6 +988,10 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         d.rank_bits = v.rank_bits;
         const double2* src = v.psi;
         if (l.d.xglob) src = e->comm ? scratch : psi + ((uint64_t(sh) ^ (l.d.xglob >> nloc)) << nloc);
+        if (l.d.xglob && emulate) {  // partner shard -> scratch, as fetch_partner does over NCCL
+          CK(cudaMemcpyAsync(scratch, src, shard_amps * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+          src = scratch;
+        }
         if (l.kind == L_OBS_DIRECT)
           launch_obs_direct(d, l.grid, s, v.psi, src, v.lam, dterms, v.part);
         else
@@ -1224,6 +1246,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     (k == "reg_bits" ? e->opt_reg_bits : e->opt_reg_bits_fwd) = value;
   } else if (k == "prefetch") {
     e->opt_prefetch = value != 0;
+  } else if (k == "emulate_transport") {
+    e->opt_emulate_transport = value != 0;
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;

@@ -140,3 +140,20 @@ def test_virtual_shards_expectation_and_determinism():
     a = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng)
     b = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng)
     assert np.array_equal(a.values, b.values) and a.energy == b.energy
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+@pytest.mark.parametrize("name", ["cfg5_n15", "cfg4_n16", "cfg3_n14", "nh_all_kinds_6", "cfg2_n12"])
+def test_nccl_data_path_emulated(name, shards):
+    """The NCCL engine's own data path -- half-shard pack, exchange, unpack for qubit
+    swaps; partner shard fetched into the scratch buffer for shard-flipping terms --
+    with device copies standing in for ncclSend/ncclRecv."""
+    rec = GOLD[name]
+    circ, theta, obs, inp, method = materialize(SMALL[name])
+    if circ.num_qubits - (shards.bit_length() - 1) < 2:
+        pytest.skip("shard too small")
+    eng = sv.distributed.virtual_engine(shards)
+    eng.set_option("emulate_transport", 1)
+    rep = _run(circ, theta, obs, inp, method, eng)
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
