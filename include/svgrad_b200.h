@@ -137,7 +137,7 @@ typedef struct {
   int32_t segments;          /* register-tile segments over all passes (0: shared-memory kernels) */
   int32_t reg_bits;          /* amplitudes per thread per buffer = 2^reg_bits (register kernels) */
   int32_t swaps;             /* sharded engines: qubit swaps (rank bit <-> local qubit) per sweep */
-  int32_t reserved;
+  int32_t jit_passes;        /* register-tile launches run by circuit-specialised (NVRTC) kernels */
   int64_t exchange_bytes;    /* sharded engines: bytes one shard sends to partners per sweep */
 } svg_stats;
 
@@ -160,7 +160,11 @@ int svg_engine_destroy(svg_engine* e);
 /* Launch on an external cudaStream_t (passed as void*); NULL = engine's own stream. */
 int svg_engine_set_stream(svg_engine* e, void* stream);
 /* Options: "tile_qubits" (0 = auto), "profile" (1 = per-phase CUDA-event times in svg_stats),
-   "max_gates_per_pass" (0 = auto), "kernel" (0 auto, 1 shared-memory tiles, 2 register tiles). */
+   "max_gates_per_pass" (0 = auto), "kernel" (0 auto, 1 shared-memory tiles, 2 register tiles),
+   "reg_bits" / "reg_bits_fwd" (3 or 4: 2^bits amplitudes per thread in reverse / forward passes),
+   "jit" (circuit-specialised register-tile kernels compiled at run time with NVRTC:
+   0 off, 1 auto = shards of >= 18 qubits, 2 always), "emulate_transport" (virtual engines:
+   run the NCCL data path with device copies), "prefetch" (ignored). */
 int svg_engine_set_option(svg_engine* e, const char* key, int64_t value);
 
 /* The hot path: one full adjoint sweep.  sums_out[num_params] receives the

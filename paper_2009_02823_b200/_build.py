@@ -15,7 +15,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsvgb200.so")
-SOURCES = ["engine.cu", "kernels.cu", "kernels_reg.cu", "plan.cpp"]
+SOURCES = ["engine.cu", "kernels.cu", "kernels_reg.cu", "jit.cu", "plan.cpp"]
+# device headers embedded into the library for the run-time compiled pass kernels (jit.cu)
+JIT_HEADERS = [("kHdrDevice", "device.cuh"), ("kHdrTileOps", "tile_ops.cuh"), ("kHdrRegOps", "reg_ops.cuh")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,7 +42,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     tmp = os.path.join(PKG, "_obj")
     os.makedirs(tmp, exist_ok=True)
-    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", os.path.join(ROOT, "include")]
+    with open(os.path.join(tmp, "jit_headers.inc"), "w") as f:
+        for name, fname in JIT_HEADERS:
+            with open(os.path.join(CSRC, fname)) as h:
+                text = h.read()
+            assert ")SVGB\"" not in text
+            f.write(f'static const char {name}[] = R"SVGB({text})SVGB";\n')
+    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", os.path.join(ROOT, "include"), "-I", tmp]
     for src in SOURCES:
         obj = os.path.join(tmp, src + ".o")
         cmd = [nvcc(), *ARCH, *common, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
@@ -50,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp_lib = LIB + ".tmp"
-    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp_lib, *objs, "-lcudart"], check=True)
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp_lib, *objs, "-lcudart", "-ldl"], check=True)
     os.replace(tmp_lib, LIB)
     return LIB
 

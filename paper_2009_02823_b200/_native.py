@@ -75,7 +75,7 @@ class svg_stats(C.Structure):
         ("fwd_passes", C.c_int32), ("obs_passes", C.c_int32), ("rev_passes", C.c_int32),
         ("tile_qubits", C.c_int32), ("pass_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64), ("segments", C.c_int32), ("reg_bits", C.c_int32),
-        ("swaps", C.c_int32), ("reserved", C.c_int32), ("exchange_bytes", C.c_int64),
+        ("swaps", C.c_int32), ("jit_passes", C.c_int32), ("exchange_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -1,7 +1,15 @@
 // Device-side data structures shared by the pass kernels and the engine.
 #pragma once
+#ifdef __CUDACC_RTC__  // run-time compiled pass kernels (jit.cpp): no host headers
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace svgb {
 
@@ -127,8 +135,11 @@ struct SegDesc {
   int32_t same_map;          // SEG_REG: identical layout to the previous register segment
   uint8_t regpos[8];         // tile positions of register bits
   uint8_t warppos[8];        // tile positions of warp bits
+  double scale;              // SEG_REG: deferred scale C of the register tile at the segment's end
+                             // (product of the scaled ops' a since the last flush; kernels_reg.cu upd)
+  double pad_;
 };
-static_assert(sizeof(SegDesc) == 32, "SegDesc layout");
+static_assert(sizeof(SegDesc) == 48, "SegDesc layout");
 
 // Entry of the finalize map: deterministic sum of `count` partials at `off`.
 struct SumSpec {

@@ -18,12 +18,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "../../include/svgrad_b200.h"
 #include "device.cuh"
+#include "jit.h"
 #include "kernels.h"
 #include "nccl_shim.h"
 #include "plan.h"
@@ -118,6 +120,7 @@ struct Launch {
   int R = 3;           // L_REG: register bits
   bool tiles = false;  // L_REG: stages the tile through shared memory
   int gbit = 0, lpos = 0;  // L_SWAP: rank bit <-> local position
+  std::shared_ptr<JitKernel> jit;  // L_REG: circuit-specialised kernel (jit.cu), or null: interpreter
 };
 
 // Everything a sweep needs on the host side, built from one svg_problem.
@@ -158,6 +161,10 @@ struct svg_engine {
   // virtual engines: run the NCCL-mode data path (half-shard pack -> copy ->
   // unpack, partner fetch into scratch) with device copies as the transport
   int64_t opt_emulate_transport = 0;
+  // circuit-specialised register-tile kernels (jit.cu): 0 off, 1 auto (shards of
+  // >= kJitMinQubits qubits), 2 always
+  int64_t opt_jit = 1;
+  mutable std::string jit_error;  // why auto mode fell back to the interpreted kernels
   DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
   // sharding: the state is split over 2^shard_bits shards by its top physical
@@ -333,6 +340,7 @@ SegDesc make_seg(int kind, uint32_t regmask, int k, int R, SegLocal* sl) {
   sl->R = R;
   SegDesc sd;
   std::memset(&sd, 0, sizeof(sd));
+  sd.scale = 1.0;
   sd.kind = kind;
   int r = 0, w = 0;
   for (int pos = 0; pos < k; ++pos) {
@@ -349,10 +357,22 @@ SegDesc make_seg(int kind, uint32_t regmask, int k, int R, SegLocal* sl) {
   return sd;
 }
 
+// Smallest |a| whose 1/a the scaled register form may carry (|t| = |b/a| <= 1e3:
+// the scaled form v + t P v has the same rounding error as a v + b P v, and the
+// host keeps the deferred scale C of a tile inside [1e-60, 1]).
+constexpr double kMinDeferredA = 1e-3;
+constexpr double kMinDeferredC = 1e-60;
+// Auto mode compiles circuit-specialised kernels for shards of at least this
+// many qubits (smaller states: the one-off compile outweighs the pass time).
+constexpr int kJitMinQubits = 18;
+
 // One register op for gate g: operator coefficients `c` (a, b of a I + b P),
 // optionally fused with the post-gate generator `kpost` into `slot`.
+// `cs` is the register tile's deferred scale C (tile = state / C) before the op:
+// an uncontrolled rotation runs in the scaled form  v + (b/a) P v  and multiplies
+// C by a; its inner-product coefficients carry C^2 (phi and lambda share C).
 void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate& g, uint32_t kind,
-              const svg_c128* c, const svg_c128* kpost, uint32_t slot, bool real_sums) {
+              const svg_c128* c, const svg_c128* kpost, uint32_t slot, bool real_sums, double* cs) {
   RegOp op;
   std::memset(&op, 0, sizeof(op));
   const int R = sl.R;
@@ -419,18 +439,36 @@ void emit_rop(Lowered& L, const TileMap& tm, const SegLocal& sl, const svg_gate&
   }
   // pure Pauli (X/Y/Z, CX, ...): a signed permutation without arithmetic
   const bool perm = op.a == 0.0 && std::fabs(op.bb) == 1.0 && !kpost;
-  uint32_t mode = perm ? 2 + (bi ? 1 : 0) : (bi ? 1 : 0);
-  if (kind == ROP_REV) {
+  uint32_t mode = perm ? 2 + (bi ? 1 : 0) : (bi ? 1 : 0);  // forward kernel modes
+  if (kind == ROP_REV) {                                    // reverse kernel modes
     if (op.flags & RF_IP3)
-      mode = 6;
+      mode = 2;
     else if (op.flags & RF_IP1)
-      mode = 4 + (bi ? 1 : 0);
+      mode = bi ? 1 : 0;
     else if (perm)
-      mode = 7 + (bi ? 1 : 0);
+      mode = 3 + (bi ? 1 : 0);
     else
       throw std::logic_error("parameter-free non-permutation Pauli op reached the register path");
   }
-  op.variant = pattern + NP * ((cloc != 0) + 2 * mode);
+  // inner products see the tile before this op: scale by C^2
+  const double c2 = (*cs) * (*cs);
+  op.kr *= c2;
+  op.ka = make_double2(op.ka.x * c2, op.ka.y * c2);
+  op.kb = make_double2(op.kb.x * c2, op.kb.y * c2);
+  bool ctrl = cloc != 0;
+  if (!perm && !ctrl) {
+    if (op.co == 0 && std::fabs(op.a) >= kMinDeferredA && std::fabs(*cs * op.a) >= kMinDeferredC) {
+      // scaled form: v + t P v, C *= a
+      op.bb /= op.a;
+      *cs *= op.a;
+    } else {  // controlled by a non-tile qubit (skipped on some tiles) or tiny a: unscaled form
+      ctrl = true;
+      op.flags |= RF_CTRL;
+      op.cmask = (R >= 5) ? ~0u : ((1u << (1u << R)) - 1u);
+      op.clw = 0;
+    }
+  }
+  op.variant = pattern + NP * ((ctrl ? 1 : 0) + 2 * mode);
   L.rops.push_back(op);
 }
 
@@ -568,15 +606,18 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     } else {
       Launch l = reg_launch(ps, 1);
       uint32_t prev = ~0u;
+      double C = 1.0;  // deferred scale; flushed when the layout changes (see SegDesc.scale)
       for (const Segment& sg : psegs_f[si]) {
         SegLocal sl;
         SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF), L.k, RF, &sl);
         sd.same_map = sg.reg && sg.regmask == prev;
         prev = sg.reg ? sg.regmask : ~0u;
+        if (!sd.same_map) C = 1.0;
         if (sg.reg) {
           sd.op_begin = static_cast<int>(L.rops.size());
-          for (int it : sg.items) emit_rop(L, tm, sl, gs[it], ROP_FWD, gs[it].fwd, nullptr, 0, real_sums);
+          for (int it : sg.items) emit_rop(L, tm, sl, gs[it], ROP_FWD, gs[it].fwd, nullptr, 0, real_sums, &C);
           sd.op_end = static_cast<int>(L.rops.size());
+          sd.scale = C;
         } else {
           sd.op_begin = static_cast<int>(L.ops.size());
           for (int it : sg.items) emit_op(L, tm, gs[it], OP_APPLY_PAULI, 0, gs[it].fwd, 0);
@@ -701,12 +742,14 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         Launch l = reg_launch(ps, 2);
         const std::vector<Segment>& sgs = psegs[si];
         uint32_t prev = ~0u;
+        double C = 1.0;
         for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
           const Segment& sg = *st;
           SegLocal sl;
           SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RB), L.k, RB, &sl);
           sd.same_map = sg.reg && sg.regmask == prev;
           prev = sg.reg ? sg.regmask : ~0u;
+          if (!sd.same_map) C = 1.0;
           if (sg.reg) {
             sd.op_begin = static_cast<int>(L.rops.size());
             for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it) {
@@ -720,9 +763,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
               }
               // one op rewinds phi AND lambda (rewind == adjoint for register-capable gates);
               // the reference skips lambda's update at i = 0, whose value is never read again
-              emit_rop(L, tm, sl, gt, ROP_REV, gt.rewind, kpost, kpost ? slot++ : 0, real_sums);
+              emit_rop(L, tm, sl, gt, ROP_REV, gt.rewind, kpost, kpost ? slot++ : 0, real_sums, &C);
             }
             sd.op_end = static_cast<int>(L.rops.size());
+            sd.scale = C;
           } else {
             sd.op_begin = static_cast<int>(L.ops.size());
             for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it)
@@ -761,9 +805,19 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       case L_REG:
         // per-thread inner-product accumulators when they fit a modest budget
         l.d.thread_acc = l.nb == 2 && size_t(l.d.nslots) * l.threads * sizeof(double) <= (48u << 10);
-        l.d.prefetch = e->opt_prefetch != 0;
-        l.smem = reg_smem(L.k, l.d.b, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin, l.tiles,
-                          l.d.thread_acc != 0, l.d.prefetch != 0);
+        if (l.jit) {
+          l.smem = l.jit->smem;
+          int blocks = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, reinterpret_cast<const void*>(l.jit->fn),
+                                                            l.threads, l.smem) != cudaSuccess || blocks < 1) {
+            (void)cudaGetLastError();
+            blocks = 1;
+          }
+          l.grid = clamp_grid(blocks);
+          break;
+        }
+        l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin,
+                          l.d.seg_end - l.d.seg_begin, l.tiles, l.d.thread_acc != 0);
         l.grid = clamp_grid(reg_occupancy(l.nb, l.R, l.threads, l.smem));
         break;
       case L_OBS:
@@ -780,6 +834,44 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     }
     if (l.smem > e->max_smem) throw InvalidArg("pass needs more shared memory than the device offers");
   };
+  // circuit-specialised kernels for the register-tile passes
+  const bool want_jit = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits));
+  if (want_jit) {
+    std::vector<Launch*> regl;
+    for (std::vector<Launch>* v : {&L.fwd, &L.rev})
+      for (Launch& l : *v)
+        if (l.kind == L_REG) regl.push_back(&l);
+    std::vector<JitPass> passes;
+    passes.reserve(regl.size());
+    for (Launch* l : regl) {
+      l->d.thread_acc = l->nb == 2 && size_t(l->d.nslots) * l->threads * sizeof(double) <= (48u << 10);
+      JitPass jp;
+      jp.R = l->R;
+      jp.nb = l->nb;
+      jp.k = L.k;
+      jp.nloc = nloc;
+      jp.threads = l->threads;
+      jp.nslots = l->d.nslots;
+      jp.thread_acc = l->d.thread_acc != 0;
+      jp.tiles = l->tiles;
+      jp.rest = l->d.rest;
+      jp.q = l->d.q;
+      jp.segs = L.segs.data() + l->d.seg_begin;
+      jp.nsegs = l->d.seg_end - l->d.seg_begin;
+      jp.rops = L.rops.data() + l->d.op_begin;
+      jp.op_begin = l->d.op_begin;
+      passes.push_back(jp);
+    }
+    try {
+      std::string why;
+      if (!jit_available(&why)) throw std::runtime_error(why);
+      std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->device);
+      for (size_t i = 0; i < regl.size(); ++i) regl[i]->jit = ks[i];
+    } catch (const std::exception& ex) {
+      if (e->opt_jit == 2) throw;
+      e->jit_error = ex.what();  // auto: keep the interpreted kernels
+    }
+  }
   for (Launch& l : L.fwd) size_launch(l);
   for (Launch& l : L.obs) {
     size_launch(l);
@@ -943,6 +1035,20 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       nccl->check(nccl->group_end(), "ncclGroupEnd");
     };
 
+    int jit_launches = 0;
+    // register-tile pass: the circuit-specialised kernel when there is one, else the interpreter
+    auto launch_reg = [&](const Launch& l, const PassDesc& d, double2* b0, double2* b1, double2* prt) {
+      if (!l.jit) {
+        launch_pass_reg(l.nb, l.R, d, l.grid, l.threads, l.smem, s, b0, b1, dsegs, drops, dops, dcoef, prt);
+        return;
+      }
+      const JitArgsHead head{b0, b1, dops, dcoef, prt, d.part_off, d.rank_bits};
+      std::vector<unsigned char> args =
+          jit_args(*l.jit, head, L.segs.data() + d.seg_begin, L.rops.data() + d.op_begin);
+      void* params[] = {args.data()};
+      CK(cudaLaunchKernel(reinterpret_cast<const void*>(l.jit->fn), dim3(l.grid), dim3(l.threads), params, l.smem, s));
+      ++jit_launches;
+    };
     int64_t launches = 0, h2d = bl.total, d2h = 0;
     CK(cudaEventRecord(e->ev[0], s));
     CK(cudaMemcpyAsync(db, hb, bl.total, cudaMemcpyHostToDevice, s));
@@ -970,7 +1076,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         PassDesc d = l.d;
         d.rank_bits = v.rank_bits;
         if (l.kind == L_REG)
-          launch_pass_reg(1, l.R, d, l.grid, l.threads, l.smem, s, v.psi, nullptr, dsegs, drops, dops, dcoef, v.part);
+          launch_reg(l, d, v.psi, nullptr, v.part);
         else
           launch_fwd(d, l.grid, l.smem, s, v.psi, dops, dcoef);
         ++launches;
@@ -1011,7 +1117,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         PassDesc d = l.d;
         d.rank_bits = v.rank_bits;
         if (l.kind == L_REG)
-          launch_pass_reg(2, l.R, d, l.grid, l.threads, l.smem, s, v.psi, v.lam, dsegs, drops, dops, dcoef, v.part);
+          launch_reg(l, d, v.psi, v.lam, v.part);
         else
           launch_rev(d, l.grid, l.smem, s, v.psi, v.lam, dops, dcoef, v.part);
         ++launches;
@@ -1086,6 +1192,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       stats->d2h_bytes = d2h;
       stats->swaps = L.swaps;
       stats->exchange_bytes = L.swap_bytes;
+      stats->jit_passes = jit_launches;
     }
     return SVG_OK;
   } catch (const InvalidArg& ex) {
@@ -1244,13 +1351,16 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     if (value == 0) value = 4;
     if (value != 3 && value != 4) return fail(SVG_EINVAL, k + " must be 3 or 4");
     (k == "reg_bits" ? e->opt_reg_bits : e->opt_reg_bits_fwd) = value;
-  } else if (k == "prefetch") {
+  } else if (k == "prefetch") {  // accepted for compatibility; the bulk-copy tile prefetch was removed
     e->opt_prefetch = value != 0;
   } else if (k == "emulate_transport") {
     e->opt_emulate_transport = value != 0;
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;
+  } else if (k == "jit") {
+    if (value < 0 || value > 2) return fail(SVG_EINVAL, "jit must be 0 (off), 1 (auto) or 2 (always)");
+    e->opt_jit = value;
   } else if (k == "max_gates_per_pass") {
     if (value < 0) return fail(SVG_EINVAL, "max_gates_per_pass must be >= 0");
     e->opt_max_items = value;

@@ -196,17 +196,22 @@ __global__ void __launch_bounds__(kThreads) k_rev_pass(double2* __restrict__ phi
   }
 }
 
+// One warp per sum: lane l adds partials l, l+32, ... in order, then a fixed
+// shuffle tree -- the same order on every run (deterministic), 32x the
+// memory-level parallelism of a thread per sum.
 __global__ void k_finalize(const double2* __restrict__ partials, const SumSpec* __restrict__ specs,
                            int count, double2* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= count) return;
   const SumSpec sp = specs[i];
   double2 acc = make_double2(0.0, 0.0);
-  for (int64_t c = 0; c < sp.count; ++c) {
+  for (int64_t c = lane; c < sp.count; c += 32) {
     const double2 v = partials[sp.off + c];
     acc = make_double2(acc.x + v.x, acc.y + v.y);
   }
-  out[i] = acc;
+  acc = warp_sum(acc);
+  if (lane == 0) out[i] = acc;
 }
 
 __global__ void k_set_basis(double2* psi, uint64_t idx) { psi[idx] = make_double2(1.0, 0.0); }
@@ -293,7 +298,7 @@ void launch_rev(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double
 void launch_finalize(const double2* partials, const SumSpec* specs, int count, double2* out,
                      cudaStream_t s) {
   if (count <= 0) return;
-  k_finalize<<<(count + 127) / 128, 128, 0, s>>>(partials, specs, count, out);
+  k_finalize<<<(count + 3) / 4, 128, 0, s>>>(partials, specs, count, out);  // 4 sums (warps) per block
 }
 void launch_set_basis(double2* psi, uint64_t idx, cudaStream_t s) { k_set_basis<<<1, 1, 0, s>>>(psi, idx); }
 

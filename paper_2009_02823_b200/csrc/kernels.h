@@ -34,7 +34,7 @@ void launch_finalize(const double2* partials, const SumSpec* specs, int count, d
 void launch_set_basis(double2* psi, uint64_t idx, cudaStream_t s);
 
 // register-tile passes (kernels_reg.cu)
-size_t reg_smem(int k, int b, int nb, int nwarps, int nslots, int nops, bool tiles, bool thread_acc, bool prefetch);
+size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, int nsegs, bool tiles, bool thread_acc);
 cudaError_t prepare_reg_kernels(size_t max_smem);
 int reg_occupancy(int nb, int R, int threads, size_t smem);
 int reg_max_threads(int R);

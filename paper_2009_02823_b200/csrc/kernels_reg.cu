@@ -21,322 +21,79 @@
 
 #include "device.cuh"
 #include "kernels.h"
+#include "reg_ops.cuh"
 #include "tile_ops.cuh"
 
 namespace svgb {
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRegThreads = 256;  // launch bound: k = 11 tiles with R = 3 (8 warps)
 
-__device__ __forceinline__ double2 shfl2(double2 v, uint32_t m) {
-  return make_double2(__shfl_xor_sync(kFull, v.x, m), __shfl_xor_sync(kFull, v.y, m));
-}
-// flip the sign of both components when bit `s` (0/1) is set (sign-bit xor, no FP op)
-__device__ __forceinline__ double2 sflip(double2 v, uint32_t s) {
-  const long long m = static_cast<long long>(s) << 63;
-  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
-                      __longlong_as_double(__double_as_longlong(v.y) ^ m));
-}
-
-// ---- async bulk copies (TMA engine, cp.async.bulk) completing on an mbarrier ----
-__device__ __forceinline__ uint32_t saddr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n}" ::"r"(saddr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
-      "l"(src), "r"(bytes), "r"(saddr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// Warp 0 streams tile `base` (rows of 2^b contiguous amplitudes) into the stage buffers.
-template <int NB>
-__device__ __forceinline__ void prefetch_tile(const PassDesc& d, const uint64_t* rows, uint64_t base,
-                                              const double2* b0, const double2* b1, double2* st0, double2* st1,
-                                              uint64_t* bar) {
-  // one elected thread issues every row (the bulk-copy operands live in uniform registers)
-  if ((threadIdx.x & 31) != 0) return;
-  const int nrows = 1 << (d.k - d.b);
-  const uint32_t row_bytes = uint32_t(sizeof(double2)) << d.b;
-  fence_async_smem();  // order earlier generic-proxy smem accesses before the async writes
-  mbar_expect_tx(bar, uint32_t(NB) * uint32_t(nrows) * row_bytes);
-  for (int r = 0; r < nrows; ++r) {
-    const uint64_t g = base | rows[r];
-    bulk_g2s(st0 + (size_t(r) << d.b), b0 + g, row_bytes, bar);
-    if (NB == 2) bulk_g2s(st1 + (size_t(r) << d.b), b1 + g, row_bytes, bar);
-  }
-}
-
-template <int R>
-struct Map {
-  uint64_t gw;        // global offset of this warp's warp bits
-  uint64_t gbit[R];   // global offset of register bit i
-  uint32_t sw;        // tile-local offset of the warp bits
-  uint32_t sbit[R];   // tile-local offset of register bit i
-};
-
-template <int R>
-__device__ __forceinline__ void make_map(Map<R>& m, const SegDesc& sg, const uint8_t* sq, int warp, int wbits) {
-  m.gw = 0;
-  m.sw = 0;
-  for (int i = 0; i < wbits; ++i)
-    if ((warp >> i) & 1) {
-      m.gw |= 1ull << sq[sg.warppos[i]];
-      m.sw |= 1u << sg.warppos[i];
-    }
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    m.gbit[i] = 1ull << sq[sg.regpos[i]];
-    m.sbit[i] = 1u << sg.regpos[i];
-  }
-}
-
-template <int R>
-__device__ __forceinline__ uint64_t goff(const Map<R>& m, int j) {
-  uint64_t o = 0;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if ((j >> i) & 1) o |= m.gbit[i];
-  return o;
-}
-template <int R>
-__device__ __forceinline__ uint32_t soff(const Map<R>& m, int j) {
-  uint32_t o = 0;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if ((j >> i) & 1) o |= m.sbit[i];
-  return o;
-}
-
-template <int R>
-__device__ __forceinline__ void load_g(double2 (&v)[1 << R], const double2* __restrict__ g, uint64_t row,
-                                       const Map<R>& m) {
-#pragma unroll
-  for (int j = 0; j < (1 << R); ++j) v[j] = g[row | goff(m, j)];
-}
-template <int R>
-__device__ __forceinline__ void store_g(const double2 (&v)[1 << R], double2* __restrict__ g, uint64_t row,
-                                        const Map<R>& m) {
-#pragma unroll
-  for (int j = 0; j < (1 << R); ++j) g[row | goff(m, j)] = v[j];
-}
-template <int R>
-__device__ __forceinline__ void to_smem(const double2 (&v)[1 << R], double2* s, uint32_t row, const Map<R>& m) {
-#pragma unroll
-  for (int j = 0; j < (1 << R); ++j) s[row | soff(m, j)] = v[j];
-}
-template <int R>
-__device__ __forceinline__ void from_smem(double2 (&v)[1 << R], const double2* s, uint32_t row, const Map<R>& m) {
-#pragma unroll
-  for (int j = 0; j < (1 << R); ++j) v[j] = s[row | soff(m, j)];
-}
-
-// Per-op, per-thread constants.
-struct OpCtx {
-  double a, bb;    // new = a v + bb * (i^BI) * p   (bb carries the uniform part of the partner sign)
-  double2 bc;      // generic complex b' (reverse mode 6)
-  uint32_t pneg;   // permutation modes: sign of bb (bb = +-1)
-  uint32_t smask;  // register part of the partner sign (runtime patterns only)
-  uint32_t cmask;  // register part of the control test
-  bool clw_ok;     // lane/warp part of the control test
-};
-
-// Register-op patterns: flip shape and how the partner sign depends on the
-// register slot j.  Compile-time sign patterns cost nothing (negated FMA
-// operands); only the rare multi-bit Z patterns read the runtime smask.
-//   P_DIAG            diagonal, sign uniform
-//   P_DIAGZ + b       diagonal, sign_j = bit_b(j)               (RZ-type on register bit b)
-//   P_LANE            lane flip, sign uniform
-//   P_REG + b         flip register bit b, sign uniform         (RX-type)
-//   P_REGY + b        flip register bit b, sign_j = !bit_b(j)   (RY-type: Z on the flipped bit)
-//   P_GDIAG / P_GLANE / P_GREG + b   runtime smask
-template <int R>
-struct Pat {
-  static constexpr int DIAG = 0, DIAGZ = 1, LANE = 1 + R, REG = 2 + R, REGY = 2 + 2 * R, GDIAG = 2 + 3 * R,
-                       GLANE = 3 + 3 * R, GREG = 4 + 3 * R, N = 4 + 4 * R;
-};
-
-// v <- a v + (-1)^neg bb (i^BI p)      (in-place friendly: the DFMA overwrites v)
-template <int BI>
-__device__ __forceinline__ double2 upd(const OpCtx& c, double2 v, double2 p, bool neg) {
-  if (BI >= 3) {  // pure Pauli (a = 0, |b'| = 1): a signed permutation, no arithmetic
-    const uint32_t s = uint32_t(neg) ^ c.pneg;
-    return BI == 3 ? sflip(p, s) : sflip(make_double2(-p.y, p.x), s);
-  }
-  double tx, ty;
-  if (BI == 1) {
-    tx = -c.bb * p.y;
-    ty = c.bb * p.x;
-  } else if (BI == 0) {
-    tx = c.bb * p.x;
-    ty = c.bb * p.y;
-  } else {
-    tx = fma(c.bc.x, p.x, -c.bc.y * p.y);
-    ty = fma(c.bc.x, p.y, c.bc.y * p.x);
-  }
-  if (neg) {
-    tx = -tx;
-    ty = -ty;
-  }
-  return make_double2(fma(c.a, v.x, tx), fma(c.a, v.y, ty));
-}
-
-// Inner-product terms for one amplitude: partner p with sign (-1)^neg.
-// IPK 1: q += Re(conj(lam) sel(s p)), sel = -i (BI) or 1 ; IPK 3: z += conj(lam) s p, z2 += conj(lam) v.
-template <int IPK, int BI>
-__device__ __forceinline__ void ip_term(double2 lam, double2 p, double2 v, bool neg, double& q, double2& z,
-                                        double2& z2) {
-  const double lx = neg ? -lam.x : lam.x, ly = neg ? -lam.y : lam.y;  // sign folded into lambda (free negation)
-  if (IPK == 1) {
-    if (BI == 1)
-      q = fma(lx, p.y, fma(-ly, p.x, q));
-    else
-      q = fma(lx, p.x, fma(ly, p.y, q));
-  } else if (IPK == 3) {
-    z.x = fma(lx, p.x, fma(ly, p.y, z.x));
-    z.y = fma(lx, p.y, fma(-ly, p.x, z.y));
-    z2.x = fma(lam.x, v.x, fma(lam.y, v.y, z2.x));
-    z2.y = fma(lam.x, v.y, fma(-lam.y, v.x, z2.y));
-  }
-}
-
-// Sign of the partner of register slot j for pattern P (compile-time unless runtime pattern).
-template <int R, int P>
-__device__ __forceinline__ bool psign(const OpCtx& c, int j) {
-  using PT = Pat<R>;
-  if constexpr (P >= PT::DIAGZ && P < PT::LANE) return (j >> (P - PT::DIAGZ)) & 1;
-  else if constexpr (P >= PT::REGY && P < PT::GDIAG) return !((j >> (P - PT::REGY)) & 1);
-  else if constexpr (P >= PT::GDIAG) return (c.smask >> j) & 1u;
-  else return false;
-}
-
-// One op on the register tile v (and, DUAL, the same op on lambda l).  For
-// IPK != 0 the inner product uses lambda and phi before the update (phi_{i+1}).
-template <int R, int P, int IPK, int BI, bool CTRL, bool DUAL>
-__device__ __forceinline__ void reg_op(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
-                                       double& q0, double& q1, double2& z, double2& z2) {
-  using PT = Pat<R>;
-  constexpr int NR = 1 << R;
-  constexpr bool LANEF = (P == PT::LANE || P == PT::GLANE);
-  constexpr int XB = (P >= PT::REG && P < PT::GDIAG) ? (P - PT::REG) % R : (P >= PT::GREG ? P - PT::GREG : -1);
-  constexpr int XR = XB >= 0 ? (1 << XB) : 0;
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    if (XR != 0 && (j & XR)) continue;  // register pairs handled at the low member
-    const int jp = j ^ XR;
-    const bool sj = psign<R, P>(c, j);
-    const bool okj = !CTRL || (c.clw_ok && ((c.cmask >> j) & 1u));
-    double2 pj = v[jp];  // partner of slot j (slot jp of the partner lane)
-    double2 lpj = DUAL ? l[jp] : pj;
-    if (LANEF) {
-      pj = shfl2(pj, xl);
-      if (DUAL) lpj = shfl2(lpj, xl);
-    }
-    if (IPK != 0 && okj) ip_term<IPK, BI>(l[j], pj, v[j], sj, (j & 1) ? q1 : q0, z, z2);
-    if (XR == 0) {
-      if (!CTRL || okj) {
-        v[j] = upd<BI>(c, v[j], pj, sj);
-        if (DUAL) l[j] = upd<BI>(c, l[j], lpj, sj);
-      }
-    } else {
-      const bool sp = psign<R, P>(c, jp);
-      if (IPK != 0 && okj) ip_term<IPK, BI>(l[jp], v[j], v[jp], sp, q1, z, z2);
-      if (!CTRL || okj) {
-        const double2 vj = v[j], lj = l[j];
-        v[j] = upd<BI>(c, vj, pj, sj);
-        v[jp] = upd<BI>(c, v[jp], vj, sp);
-        if (DUAL) {
-          l[j] = upd<BI>(c, lj, lpj, sj);
-          l[jp] = upd<BI>(c, l[jp], lj, sp);
-        }
-      }
-    }
-  }
-}
-
-// Flat variant id (computed on the host, see engine.cu emit_rop):
-//   id = pattern + Pat<R>::N * (ctrl + 2 * mode)
-//   mode: forward 0/1 (BI 0/1), 2/3 (signed permutation, BI 0/1: pure Pauli X/Y/Z, CX...);
-//         reverse 4/5 (IPK 1, BI 0/1), 6 (IPK 3, generic complex coefficients),
-//         7/8 (signed permutation on phi and lambda, BI 0/1)
-constexpr int kModes = 9;
 template <int R, int NB, int V>
-__device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
-                                            double& q0, double& q1, double2& z, double2& z2) {
-  constexpr int NP = Pat<R>::N;
-  if constexpr (V < NP * 2 * kModes) {
-    constexpr int P = V % NP;
-    constexpr bool CTRL = (V / NP) % 2;
-    constexpr int mode = V / NP / 2;
-    constexpr bool DUAL = mode >= 4;
-    constexpr int IPK = mode == 6 ? 3 : ((mode == 4 || mode == 5) ? 1 : 0);
-    constexpr int BI = mode == 6 ? 2 : (mode == 2 || mode == 7) ? 3 : (mode == 3 || mode == 8) ? 4 : (mode & 1);
-    // forward kernels only hold forward modes, reverse kernels only reverse modes (code size)
-    if constexpr ((NB == 2) == DUAL) reg_op<R, P, IPK, BI, CTRL, DUAL>(v, l, c, xl, q0, q1, z, z2);
-  }
+__device__ __forceinline__ void run_variant(double2 (&v)[1 << R], double2 (&l)[1 << R], const RegOp& op,
+                                            const OpCtx& c, uint32_t slw, const IpSink& sink) {
+  op_body<R, NB, V>(v, l, c, op.xl, slw, (op.flags & RF_BI) != 0, op.slot, op.kr, op.ka, op.kb, sink);
 }
 
 #define SVGB_V1(N) \
   case (N):        \
-    run_variant<R, NB, (N)>(v, l, c, xl, q0, q1, z, z2); \
+    run_variant<R, NB, (N)>(v, l, op, c, slw, sink); \
     break;
 #define SVGB_V4(N) SVGB_V1(N) SVGB_V1(N + 1) SVGB_V1(N + 2) SVGB_V1(N + 3)
-#define SVGB_V16(N) SVGB_V4(N) SVGB_V4(N + 4) SVGB_V4(N + 8) SVGB_V4(N + 12)
-#define SVGB_V64(N) SVGB_V16(N) SVGB_V16(N + 16) SVGB_V16(N + 32) SVGB_V16(N + 48)
+#define SVGB_V20(N) SVGB_V4(N) SVGB_V4(N + 4) SVGB_V4(N + 8) SVGB_V4(N + 12) SVGB_V4(N + 16)
 
+// Dense switch over exactly the kernel's variants (a single jump table).
 template <int R, int NB>
-__device__ __forceinline__ void dispatch(uint32_t id, double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c,
-                                         uint32_t xl, double& q0, double& q1, double2& z, double2& z2) {
-  static_assert(Pat<R>::N * 2 * kModes <= 384, "extend the dispatch table");
-  switch (id) {
-    SVGB_V64(0)
-    SVGB_V64(64)
-    SVGB_V64(128)
-    SVGB_V64(192)
-    SVGB_V64(256)
-    SVGB_V64(320)
-    default:
-      break;
+__device__ __forceinline__ void dispatch(uint32_t id, double2 (&v)[1 << R], double2 (&l)[1 << R], const RegOp& op,
+                                         OpCtx& c, uint32_t slw, const IpSink& sink) {
+  constexpr int NV = Pat<R>::N * 2 * (NB == 2 ? kRevModes : kFwdModes);
+  static_assert(NV % 20 == 0 || NV % 4 == 0, "variant count");
+  if constexpr (R == 4) {  // N = 20
+    if constexpr (NB == 1) {
+      static_assert(NV == 160, "");
+      switch (id) {
+        SVGB_V20(0) SVGB_V20(20) SVGB_V20(40) SVGB_V20(60) SVGB_V20(80) SVGB_V20(100) SVGB_V20(120) SVGB_V20(140)
+        default: break;
+      }
+    } else {
+      static_assert(NV == 200, "");
+      switch (id) {
+        SVGB_V20(0) SVGB_V20(20) SVGB_V20(40) SVGB_V20(60) SVGB_V20(80) SVGB_V20(100) SVGB_V20(120) SVGB_V20(140)
+        SVGB_V20(160) SVGB_V20(180)
+        default: break;
+      }
+    }
+  } else {  // R == 3: N = 16
+    if constexpr (NB == 1) {
+      static_assert(NV == 128, "");
+      switch (id) {
+        SVGB_V4(0) SVGB_V4(4) SVGB_V4(8) SVGB_V4(12) SVGB_V4(16) SVGB_V4(20) SVGB_V4(24) SVGB_V4(28)
+        SVGB_V4(32) SVGB_V4(36) SVGB_V4(40) SVGB_V4(44) SVGB_V4(48) SVGB_V4(52) SVGB_V4(56) SVGB_V4(60)
+        SVGB_V4(64) SVGB_V4(68) SVGB_V4(72) SVGB_V4(76) SVGB_V4(80) SVGB_V4(84) SVGB_V4(88) SVGB_V4(92)
+        SVGB_V4(96) SVGB_V4(100) SVGB_V4(104) SVGB_V4(108) SVGB_V4(112) SVGB_V4(116) SVGB_V4(120) SVGB_V4(124)
+        default: break;
+      }
+    } else {
+      static_assert(NV == 160, "");
+      switch (id) {
+        SVGB_V20(0) SVGB_V20(20) SVGB_V20(40) SVGB_V20(60) SVGB_V20(80) SVGB_V20(100) SVGB_V20(120) SVGB_V20(140)
+        default: break;
+      }
+    }
   }
 }
-#undef SVGB_V64
-#undef SVGB_V16
+#undef SVGB_V20
 #undef SVGB_V4
 #undef SVGB_V1
-
-__device__ __forceinline__ double warp_sum1(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
 
 }  // namespace
 
 template <int R, int NB>
-__global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3 ? 2 : (NB == 2 ? 2 : 4)) k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1,
-                                                             const PassDesc d, const SegDesc* __restrict__ segs,
-                                                             const RegOp* __restrict__ rops,
-                                                             const DevOp* __restrict__ ops,
-                                                             const double2* __restrict__ coef,
-                                                             double2* __restrict__ partials) {
+__global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3 ? 2 : (NB == 2 ? 2 : 4))
+    k_pass_reg(double2* __restrict__ b0, double2* __restrict__ b1, const PassDesc d, const SegDesc* __restrict__ segs,
+               const RegOp* __restrict__ rops, const DevOp* __restrict__ ops, const double2* __restrict__ coef,
+               double2* __restrict__ partials) {
   constexpr int NR = 1 << R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint8_t sq[kMaxQubits];
@@ -344,8 +101,10 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   const int nwarps = nthr >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wbits = d.k - 5 - R;
+  const int nsegs = d.seg_end - d.seg_begin;
   double2* wacc = reinterpret_cast<double2*>(smem_raw);  // [nwarps][nslots]
-  RegOp* sops = reinterpret_cast<RegOp*>(wacc + nwarps * d.nslots);  // this pass's register ops
+  SegDesc* ssegs = reinterpret_cast<SegDesc*>(wacc + nwarps * d.nslots);  // this pass's segments
+  RegOp* sops = reinterpret_cast<RegOp*>(ssegs + nsegs);                  // this pass's register ops
   const int nops = d.op_end - d.op_begin;
   double* tacc = d.thread_acc ? reinterpret_cast<double*>(sops + nops) : nullptr;  // [nslots][nthr]
   double2* st0 = reinterpret_cast<double2*>(sops + nops) + (d.thread_acc ? (d.nslots * nthr + 1) / 2 : 0);
@@ -357,22 +116,13 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
     const uint4* src = reinterpret_cast<const uint4*>(rops + d.op_begin);
     uint4* dst = reinterpret_cast<uint4*>(sops);
     for (int i = threadIdx.x; i < nops * int(sizeof(RegOp) / 16); i += nthr) dst[i] = src[i];
+    const uint4* ssrc = reinterpret_cast<const uint4*>(segs + d.seg_begin);
+    uint4* sdst = reinterpret_cast<uint4*>(ssegs);
+    for (int i = threadIdx.x; i < nsegs * int(sizeof(SegDesc) / 16); i += nthr) sdst[i] = ssrc[i];
   }
   if (threadIdx.x < kMaxQubits) sq[threadIdx.x] = d.q[threadIdx.x];
-  __shared__ uint64_t mbar;
-  uint64_t* rows = reinterpret_cast<uint64_t*>(st1 + (NB == 2 ? (1u << d.k) : 0));  // [2^(k-b)] row offsets
-  if (d.prefetch) {
-    for (int r = threadIdx.x; r < (1 << (d.k - d.b)); r += nthr) {
-      uint64_t off = 0;
-      for (int j = d.b; j < d.k; ++j)
-        if ((r >> (j - d.b)) & 1) off |= 1ull << d.q[j];
-      rows[r] = off;
-    }
-    if (threadIdx.x == 0) mbar_init(&mbar);
-  }
   __syncthreads();
-  if (d.prefetch && warp == 0) prefetch_tile<NB>(d, rows, pdep64(blockIdx.x, d.rest), b0, b1, st0, st1, &mbar);
-  uint32_t phase = 0;
+  const IpSink sink{tacc, wacc, nthr, d.nslots, warp, lane};
 
   const uint32_t tbase = uint32_t(lane) | (uint32_t(warp) << (5 + R));
   double2 v[NR], l[NR];
@@ -382,78 +132,63 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
     const uint64_t sbase = base | d.rank_bits;  // physical index bits for Z-signs / controls
-    const uint64_t next = T + gridDim.x;
-    Map<R> m;
-    make_map<R>(m, segs[d.seg_begin], sq, warp, wbits);
-    if (d.prefetch) {  // this tile was streamed into the stage buffers by the async copy engine
-      mbar_wait(&mbar, phase);
-      phase ^= 1u;
-      from_smem<R>(v, st0, lane | m.sw, m);
-      if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
-    } else {
+    int mseg = 0;  // segment whose register layout v / l are in
+    {
+      Map<R> m;
+      make_map<R>(m, ssegs[0], sq, warp, wbits);
       load_g<R>(v, b0, base | lane | m.gw, m);
       if (NB == 2) load_g<R>(l, b1, base | lane | m.gw, m);
     }
     bool in_smem = false;
-    for (int s = d.seg_begin; s < d.seg_end; ++s) {
-      const SegDesc sg = segs[s];
-      const bool last = s + 1 == d.seg_end;
+    double pend = 1.0;  // deferred scale of the register tile (see upd)
+    for (int s = 0; s < nsegs; ++s) {
+      const SegDesc& sg = ssegs[s];
       if (sg.kind == SEG_REG) {
-        if (s != d.seg_begin && (in_smem || !sg.same_map)) {
+        if (s != 0 && (in_smem || !sg.same_map)) {
           if (!in_smem) {
+            if (pend != 1.0) {
+              scale_tile<R>(v, pend);
+              if (NB == 2) scale_tile<R>(l, pend);
+            }
             __syncthreads();
+            Map<R> m;
+            make_map<R>(m, ssegs[mseg], sq, warp, wbits);
             to_smem<R>(v, st0, lane | m.sw, m);
             if (NB == 2) to_smem<R>(l, st1, lane | m.sw, m);
           }
           __syncthreads();
+          mseg = s;
+          Map<R> m;
           make_map<R>(m, sg, sq, warp, wbits);
           from_smem<R>(v, st0, lane | m.sw, m);
           if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
           in_smem = false;
         }
-        if (last && d.prefetch && next < ntiles) {  // stage buffers free: stream the next tile
-          __syncthreads();
-          if (warp == 0) prefetch_tile<NB>(d, rows, pdep64(next, d.rest), b0, b1, st0, st1, &mbar);
-        }
-        for (int o = sg.op_begin - d.op_begin; o < sg.op_end - d.op_begin; ++o) {
-          const RegOp& op = sops[o];
+        const RegOp* op_end = sops + (sg.op_end - d.op_begin);
+        for (const RegOp* po = sops + (sg.op_begin - d.op_begin); po != op_end; ++po) {
+          const RegOp& op = *po;
           if ((sbase & op.co) != op.co) continue;
           const uint32_t slw = uint32_t(__popc((tbase ^ op.xl) & op.zlw) ^ __popcll(sbase & op.zo)) & 1u;
           OpCtx c;
           c.a = op.a;
           c.bb = slw ? -op.bb : op.bb;  // uniform part of the partner sign
-          c.bc = (op.flags & RF_BI) ? make_double2(0.0, c.bb) : make_double2(c.bb, 0.0);
           c.smask = op.smask;
           c.cmask = op.cmask;
           c.clw_ok = (tbase & op.clw) == op.clw;
           c.pneg = c.bb < 0.0;
-          double q0 = 0.0, q1 = 0.0;
-          double2 z = make_double2(0.0, 0.0), z2 = make_double2(0.0, 0.0);
-          dispatch<R, NB>(op.variant, v, l, c, op.xl, q0, q1, z, z2);
-          if constexpr (NB == 2) {
-            if (op.flags & RF_IP1) {  // per-thread accumulator: no per-op warp reduction
-              const double q = op.kr * (slw ? -(q0 + q1) : q0 + q1);
-              if (tacc) {
-                tacc[op.slot * nthr + threadIdx.x] += q;
-              } else {
-                const double w = warp_sum1(q);
-                if (lane == 0) wacc[warp * d.nslots + op.slot].x += w;
-              }
-            } else if (op.flags & RF_IP3) {
-              if (slw) z = make_double2(-z.x, -z.y);
-              z = warp_sum(z);
-              z2 = warp_sum(z2);
-              const double2 contrib = cfma(op.kb, z, cmul(op.ka, z2));
-              if (lane == 0) {
-                double2& acc = wacc[warp * d.nslots + op.slot];
-                acc = make_double2(acc.x + contrib.x, acc.y + contrib.y);
-              }
-            }
-          }
+          dispatch<R, NB>(op.variant, v, l, op, c, slw, sink);
         }
+        pend = sg.scale;
       } else {  // SEG_SMEM: generic dense-matrix ops on the shared-memory tile
         if (!in_smem) {
+          if (pend != 1.0) {
+            scale_tile<R>(v, pend);
+            if (NB == 2) scale_tile<R>(l, pend);
+            pend = 1.0;
+          }
           __syncthreads();
+          Map<R> m;
+          make_map<R>(m, ssegs[mseg], sq, warp, wbits);
           to_smem<R>(v, st0, lane | m.sw, m);
           if (NB == 2) to_smem<R>(l, st1, lane | m.sw, m);
           __syncthreads();
@@ -473,18 +208,16 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
           }
           __syncthreads();
         }
-        if (last && d.prefetch) {
-          from_smem<R>(v, st0, lane | m.sw, m);
-          if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
-          in_smem = false;
-          __syncthreads();
-          if (warp == 0 && next < ntiles) prefetch_tile<NB>(d, rows, pdep64(next, d.rest), b0, b1, st0, st1, &mbar);
-        }
       }
     }
+    Map<R> m;
+    make_map<R>(m, ssegs[mseg], sq, warp, wbits);
     if (in_smem) {
       from_smem<R>(v, st0, lane | m.sw, m);
       if (NB == 2) from_smem<R>(l, st1, lane | m.sw, m);
+    } else if (pend != 1.0) {
+      scale_tile<R>(v, pend);
+      if (NB == 2) scale_tile<R>(l, pend);
     }
     store_g<R>(v, b0, base | lane | m.gw, m);
     if (NB == 2) store_g<R>(l, b1, base | lane | m.gw, m);
@@ -527,11 +260,10 @@ cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
 }
 }  // namespace
 
-size_t reg_smem(int k, int b, int nb, int nwarps, int nslots, int nops, bool tiles, bool thread_acc, bool prefetch) {
+size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, int nsegs, bool tiles, bool thread_acc) {
   const size_t tacc = thread_acc ? sizeof(double2) * ((size_t(nslots) * nwarps * 32 + 1) / 2) : 0;
-  const size_t rows = prefetch ? sizeof(uint64_t) << (k - b) : 0;
-  return sizeof(double2) * (size_t(nwarps) * nslots + ((tiles || prefetch) ? (size_t(nb) << k) : 0)) +
-         sizeof(RegOp) * nops + tacc + rows;
+  return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(SegDesc) * nsegs +
+         sizeof(RegOp) * nops + tacc;
 }
 
 int reg_max_threads(int R) { return R == 3 ? kRegThreads : kRegThreads / 2; }

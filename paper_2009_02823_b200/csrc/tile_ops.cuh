@@ -2,7 +2,9 @@
 // register-tile kernels (kernels_reg.cu): complex arithmetic, bit tricks, and
 // the generic tile-local gate/inner-product ops on a shared-memory tile.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
+#endif
 
 #include "device.cuh"
 

@@ -238,3 +238,58 @@ def test_full_size_parameter_shift(cfg):
         assert abs(rep.values[k].real - _parameter_shift(w, k)) <= 1e-9
     e = sv.circuit_expectation(w.circuit, w.theta, w.observable, sv.BasisState(w.num_qubits))
     assert abs(e - rep.energy) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg2_n12", "cfg3_n14", "cfg4_n16", "cfg5_n15", "cfg1", "family_D9_random",
+                                  "all_kinds_6_random", "nh_all_kinds_6"])
+@pytest.mark.parametrize("reg_bits", [3, 4])
+def test_circuit_specialised_kernels_match_golden(name, reg_bits):
+    """jit=2: every register-tile pass runs as a generated, NVRTC-compiled kernel."""
+    rec = GOLD[name]
+    circ, theta, obs, inp, method = materialize(SMALL[name])
+    stats = {}
+    run = (lambda: sv.non_hermitian_gradient(circ, theta, obs, inp)) if method == "non_hermitian" else \
+        (lambda: sv.reverse_mode_gradient(circ, theta, obs, inp, stats=stats))
+    rep = _with_options({"jit": 2, "reg_bits": reg_bits, "reg_bits_fwd": reg_bits, "tile_qubits": 9}, run)
+    sv._native.engine().set_option("jit", 1)
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+    if stats and circ.num_qubits >= 10:
+        assert stats["jit_passes"] > 0
+
+
+@pytest.mark.parametrize("n", [10, 12])
+@pytest.mark.parametrize("method", ["reverse", "non_hermitian"])
+def test_circuit_specialised_every_gate_kind(n, method):
+    from cases import all_kinds_circuit, mixed_observable, random_amplitudes
+    from oracle import oracle
+
+    circ = all_kinds_circuit(sv, n)
+    theta = np.random.default_rng([11, n]).uniform(-np.pi, 2 * np.pi, circ.num_params)
+    complex_obs = method == "non_hermitian"
+    obs = mixed_observable(sv, n, 5, count=12, letters="XYZ+-" if complex_obs else "XYZH", complex_coeffs=complex_obs)
+    inp = sv.StateVector(n, random_amplitudes(n, 3))
+    fn = sv.non_hermitian_gradient if complex_obs else sv.reverse_mode_gradient
+    rep = _with_options({"jit": 2, "tile_qubits": 9}, lambda: fn(circ, theta, obs, inp))
+    sv._native.engine().set_option("jit", 1)
+    if complex_obs:
+        vals, energy, _ = oracle.non_hermitian_values(circ, theta, obs, inp.amplitudes)
+    else:
+        vals, energy, _ = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 20), (3, 20), (4, 20), (5, 20)])
+def test_circuit_specialised_equals_interpreted(cfg, n):
+    w = sv.build_workload(cfg, n)
+    inp = sv.BasisState(n)
+    ref = _with_options({"jit": 0}, lambda: sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp))
+    sv._native.engine().set_option("jit", 1)
+    stats = {}
+    rep = _with_options({"jit": 2}, lambda: sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp,
+                                                                     stats=stats))
+    sv._native.engine().set_option("jit", 1)
+    assert stats["jit_passes"] > 0
+    assert max_err(rep.values, ref.values) <= 1e-11
+    assert abs(rep.energy - ref.energy) <= ENERGY_TOL
