@@ -61,7 +61,9 @@ def _args():
     ap.add_argument("--tile-qubits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0, help="reverse register tile: 2^bits amplitudes/thread (3/4)")
     ap.add_argument("--reg-bits-fwd", type=int, default=0, help="forward register tile: 2^bits amplitudes/thread")
-    ap.add_argument("--prefetch", action="store_true", help="stream tiles with cp.async.bulk into shared memory")
+    ap.add_argument("--no-stage", action="store_true", help="generated kernels: no cp.async next-tile staging")
+    ap.add_argument("--jit", type=int, default=1, help="circuit-specialised kernels: 0 off, 1 auto, 2 always")
+    ap.add_argument("--jit-blocks", type=str, default="0,0", help="generated kernels: min CTAs/SM fwd,rev (0 default)")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one state over the ranks (default for cfg 4/5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -215,7 +217,11 @@ def run_ours(args, rank, world, local_rank):
         eng.set_option("reg_bits", args.reg_bits)
     if args.reg_bits_fwd:
         eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
-    eng.set_option("prefetch", 1 if args.prefetch else 0)
+    eng.set_option("stage", 0 if args.no_stage else 1)
+    eng.set_option("jit", args.jit)
+    jb = [int(x) for x in args.jit_blocks.split(",")]
+    eng.set_option("jit_blocks_fwd", jb[0])
+    eng.set_option("jit_blocks_rev", jb[1])
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

@@ -139,6 +139,8 @@ typedef struct {
   int32_t swaps;             /* sharded engines: qubit swaps (rank bit <-> local qubit) per sweep */
   int32_t jit_passes;        /* register-tile launches run by circuit-specialised (NVRTC) kernels */
   int64_t exchange_bytes;    /* sharded engines: bytes one shard sends to partners per sweep */
+  double ms_host_lower;      /* host time: validation + lowering (plans, op tables, kernel lookup) */
+  double ms_host_prep;       /* host time: staging buffers between lowering and the first launch */
 } svg_stats;
 
 typedef struct svg_engine svg_engine;

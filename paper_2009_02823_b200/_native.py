@@ -76,6 +76,7 @@ class svg_stats(C.Structure):
         ("tile_qubits", C.c_int32), ("pass_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64), ("segments", C.c_int32), ("reg_bits", C.c_int32),
         ("swaps", C.c_int32), ("jit_passes", C.c_int32), ("exchange_bytes", C.c_int64),
+        ("ms_host_lower", C.c_double), ("ms_host_prep", C.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -164,6 +165,8 @@ struct svg_engine {
   // circuit-specialised register-tile kernels (jit.cu): 0 off, 1 auto (shards of
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
+  int64_t opt_stage = 1;  // generated kernels: stage the next tile with cp.async
+  int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   mutable std::string jit_error;  // why auto mode fell back to the interpreted kernels
   DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
@@ -854,6 +857,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       jp.nslots = l->d.nslots;
       jp.thread_acc = l->d.thread_acc != 0;
       jp.tiles = l->tiles;
+      jp.stage = e->opt_stage != 0;
+      jp.min_blocks = static_cast<int>(l->nb == 2 ? e->opt_jit_blocks_rev : e->opt_jit_blocks_fwd);
       jp.rest = l->d.rest;
       jp.q = l->d.q;
       jp.segs = L.segs.data() + l->d.seg_begin;
@@ -942,9 +947,11 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         svg_c128* deriv_out, svg_c128* energy_out, svg_stats* stats) {
   if (!e) return fail(SVG_EINVAL, "null engine");
   try {
+    const auto t_enter = std::chrono::steady_clock::now();
     validate(p);
     CK(cudaSetDevice(e->device));
     const Lowered L = lower(e, p, with_reverse);
+    const auto t_lowered = std::chrono::steady_clock::now();
     const int nloc = L.nloc;
     const int nsh = e->shards_local;       // shards held by this engine
     const size_t shard_amps = size_t(1) << nloc;
@@ -1050,6 +1057,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       ++jit_launches;
     };
     int64_t launches = 0, h2d = bl.total, d2h = 0;
+    const auto t_launch = std::chrono::steady_clock::now();
     CK(cudaEventRecord(e->ev[0], s));
     CK(cudaMemcpyAsync(db, hb, bl.total, cudaMemcpyHostToDevice, s));
     // input: shards are consecutive slices of the full index range (identity layout at the start)
@@ -1193,6 +1201,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       stats->swaps = L.swaps;
       stats->exchange_bytes = L.swap_bytes;
       stats->jit_passes = jit_launches;
+      stats->ms_host_lower = std::chrono::duration<double, std::milli>(t_lowered - t_enter).count();
+      stats->ms_host_prep = std::chrono::duration<double, std::milli>(t_launch - t_lowered).count();
     }
     return SVG_OK;
   } catch (const InvalidArg& ex) {
@@ -1358,6 +1368,11 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;
+  } else if (k == "jit_blocks_fwd" || k == "jit_blocks_rev") {
+    if (value < 0 || value > 8) return fail(SVG_EINVAL, k + " must be in [0, 8]");
+    (k == "jit_blocks_fwd" ? e->opt_jit_blocks_fwd : e->opt_jit_blocks_rev) = value;
+  } else if (k == "stage") {
+    e->opt_stage = value != 0;
   } else if (k == "jit") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "jit must be 0 (off), 1 (auto) or 2 (always)");
     e->opt_jit = value;

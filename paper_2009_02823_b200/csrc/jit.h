@@ -29,6 +29,8 @@ struct JitPass {
   int R = 4, nb = 1, k = 0, nloc = 0, threads = 0;
   int nslots = 0;
   bool thread_acc = false, tiles = false;
+  bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
+  int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
   const uint8_t* q = nullptr;        // tile qubits (PassDesc.q)
   const SegDesc* segs = nullptr;     // the pass's segments

@@ -272,6 +272,28 @@ __device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << 
 }
 
 
+// ---- asynchronous tile staging (cp.async, 16 B per copy, L1 bypass) ----
+// Each thread stages its own 2^R amplitudes of the NEXT tile into a private
+// slice of shared memory ([j][thread] layout: conflict-free 16-byte rows) while
+// it computes the current tile; cp.async.wait_all then makes them visible to
+// the same thread -- no block barrier.
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int R>
+__device__ __forceinline__ void stage_g(double2* stg, const double2* __restrict__ g, uint64_t row, const Map<R>& m,
+                                        int tid, int nthr) {
+#pragma unroll
+  for (int j = 0; j < (1 << R); ++j) cp_async16(stg + j * nthr + tid, g + row + goff(m, j));
+}
+template <int R>
+__device__ __forceinline__ void unstage(double2 (&v)[1 << R], const double2* stg, int tid, int nthr) {
+#pragma unroll
+  for (int j = 0; j < (1 << R); ++j) v[j] = stg[j * nthr + tid];
+}
+
 // One register op with its structure as template arguments (jit.cpp): the same
 // steps as the interpreted kernel's op loop, with every mask a literal.
 template <int R, int NB, int V, uint32_t XL, uint32_t ZLW, uint32_t CLW, uint32_t SMASK, uint32_t CMASK,

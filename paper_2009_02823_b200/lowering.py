@@ -192,12 +192,31 @@ def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     return gates, derivs
 
 
-def lower_terms(obs) -> np.ndarray:
+def _lower_terms(obs) -> np.ndarray:
     strings = pauli_strings(obs)
     terms = np.zeros(len(strings), dtype=TERM_DTYPE)
     for i, s in enumerate(strings):
         terms[i] = (s.coeff, s.x_mask, s.z_mask, s.n_y, 0)
     return terms
+
+
+_TERMS_CACHE: dict = {}
+
+
+def lower_terms(obs) -> np.ndarray:
+    """Pauli-expanded term table, cached per observable terms object (terms are
+    immutable tuples: a repeated gradient call on the same observable reuses it)."""
+    terms_obj = obs.terms
+    hit = _TERMS_CACHE.get(id(terms_obj))
+    if hit is not None and hit[0] is terms_obj and hit[1] == obs.num_qubits:
+        return hit[2]
+    table = _lower_terms(obs)
+    table.setflags(write=False)
+    if isinstance(terms_obj, tuple):
+        if len(_TERMS_CACHE) > 64:
+            _TERMS_CACHE.clear()
+        _TERMS_CACHE[id(terms_obj)] = (terms_obj, obs.num_qubits, table)
+    return table
 
 
 class Problem:

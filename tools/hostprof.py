@@ -1,5 +1,8 @@
 """Host-side cost breakdown of one gradient call (bind / native call / device)."""
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import time
 
 import paper_2009_02823_b200 as sv
@@ -23,4 +26,4 @@ for jit in (0, 1):
         sums, _, energy, stt = eng.reverse_sweep(pr.c, w.circuit.num_params, pr.num_derivs)
     t2 = time.perf_counter()
     print(f"jit={jit} bind {1e3*(t1-t0)/10:.3f} ms  native call {1e3*(t2-t1)/10:.3f} ms  device total {stt.ms_total:.3f} ms"
-          f"  jit_passes {stt.jit_passes}")
+          f"  jit_passes {stt.jit_passes}  lower {stt.ms_host_lower:.3f} ms  prep {stt.ms_host_prep:.3f} ms")
