@@ -65,6 +65,7 @@ def _args():
     ap.add_argument("--jit", type=int, default=1, help="circuit-specialised kernels: 0 off, 1 auto, 2 always")
     ap.add_argument("--jit-blocks", type=str, default="0,0", help="generated kernels: min CTAs/SM fwd,rev (0 default)")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one state over the ranks (default for cfg 4/5)")
+    ap.add_argument("--max-gates", type=int, default=0, help="gates per pass cap (0: planner default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -219,6 +220,7 @@ def run_ours(args, rank, world, local_rank):
         eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
     eng.set_option("stage", 0 if args.no_stage else 1)
     eng.set_option("jit", args.jit)
+    eng.set_option("max_gates_per_pass", args.max_gates)
     jb = [int(x) for x in args.jit_blocks.split(",")]
     eng.set_option("jit_blocks_fwd", jb[0])
     eng.set_option("jit_blocks_rev", jb[1])

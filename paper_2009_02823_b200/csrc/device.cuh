@@ -64,7 +64,7 @@ struct PassDesc {
   int32_t seg_begin, seg_end;  // register-tile passes: segment range
   int32_t smem_tiles;    // register-tile passes: 1 if the pass stages tiles in shared memory
   int32_t thread_acc;    // register-tile reverse passes: per-thread inner-product accumulators
-  int32_t prefetch;      // register-tile passes: stream tiles through shared memory with cp.async.bulk
+  int32_t acc_shift;     // thread_acc: each accumulator combines 2^acc_shift adjacent lanes (butterfly)
   int32_t pad1;
   // Sharded state: this shard's rank bits in the physical amplitude index
   // (ORed into the tile base for Z-signs and controls, never for addressing),

@@ -17,6 +17,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <map>
+#include <unordered_map>
+#include <tuple>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -167,7 +170,11 @@ struct svg_engine {
   int64_t opt_jit = 1;
   int64_t opt_stage = 1;  // generated kernels: stage the next tile with cp.async
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
-  mutable std::string jit_error;  // why auto mode fell back to the interpreted kernels
+  mutable std::string jit_error;
+  // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
+  mutable std::map<std::tuple<int, int, int, size_t>, int> occ_memo;
+  // segment plans are pure functions of a pass's flip / touch / dense pattern
+  mutable std::unordered_map<std::string, std::vector<Segment>> seg_memo;  // why auto mode fell back to the interpreted kernels
   DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
   // sharding: the state is split over 2^shard_bits shards by its top physical
@@ -368,6 +375,9 @@ constexpr double kMinDeferredC = 1e-60;
 // Auto mode compiles circuit-specialised kernels for shards of at least this
 // many qubits (smaller states: the one-off compile outweighs the pass time).
 constexpr int kJitMinQubits = 18;
+// Gates per register-tile pass: beyond ~40 the straight-line pass kernels
+// outgrow the instruction cache (measured: cfg 3 reverse 115 ms at 96, 105 ms at 40).
+constexpr int kRegPassGates = 40;
 
 // One register op for gate g: operator coefficients `c` (a, b of a I + b P),
 // optionally fused with the post-gate generator `kpost` into `slot`.
@@ -494,6 +504,24 @@ bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
   return __builtin_popcount(hi) == 1 && (flip_tile & 31u) == 0;
 }
 
+std::vector<Segment> memo_segments(const svg_engine* e, const std::vector<uint32_t>& flips,
+                                   const std::vector<uint32_t>& touch, const std::vector<char>& dense, int k,
+                                   int regbits) {
+  std::string key;
+  key.reserve(8 + flips.size() * 9);
+  const int32_t head[] = {k, regbits};
+  key.append(reinterpret_cast<const char*>(head), sizeof(head));
+  key.append(reinterpret_cast<const char*>(flips.data()), flips.size() * 4);
+  key.append(reinterpret_cast<const char*>(touch.data()), touch.size() * 4);
+  key.append(dense.data(), dense.size());
+  auto it = e->seg_memo.find(key);
+  if (it != e->seg_memo.end()) return it->second;
+  std::vector<Segment> segs = plan_segments(flips, touch, dense, k, regbits);
+  if (e->seg_memo.size() > 16384) e->seg_memo.clear();
+  e->seg_memo.emplace(std::move(key), segs);
+  return segs;
+}
+
 // Physical copy of a gate under the logical -> physical qubit map of its step.
 svg_gate physical_gate(const svg_gate& g, const std::vector<int>& l2p) {
   svg_gate q = g;
@@ -526,7 +554,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   pp.n = nloc;
   pp.k = L.k;
   pp.b = L.b;
-  if (e->opt_max_items > 0) pp.max_items = static_cast<int>(e->opt_max_items);
+  if (e->opt_max_items > 0)
+    pp.max_items = static_cast<int>(e->opt_max_items);
+  else if (L.reg)
+    pp.max_items = kRegPassGates;
   const int64_t S = int64_t(16) << nloc;  // bytes of one state shard
 
   std::vector<GateShape> logical(p->num_gates);
@@ -563,8 +594,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         touch[j] = tm.local(pshapes[si][j].touch);
         dense[j] = !reg_capable(pgates[si][j], flips[j]);
       }
-      psegs[si] = plan_segments(flips, touch, dense, L.k, RB);
-      psegs_f[si] = RF == RB ? psegs[si] : plan_segments(flips, touch, dense, L.k, RF);
+      psegs[si] = memo_segments(e, flips, touch, dense, L.k, RB);
+      psegs_f[si] = RF == RB ? psegs[si] : memo_segments(e, flips, touch, dense, L.k, RF);
     }
   }
   auto reg_launch = [&](const Pass& ps, int nb) {
@@ -701,6 +732,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         }
         L.terms.push_back(dt);
       }
+      if (!l.d.untiled)  // group equal flip masks (the kernel shares the partner amplitude)
+        std::stable_sort(L.terms.begin() + l.d.op_begin, L.terms.end(),
+                         [](const DevTerm& x, const DevTerm& y) { return x.xl < y.xl; });
       l.d.op_end = static_cast<int>(L.terms.size());
       l.d.accumulate = L.obs_kernels > 0;
       L.obs_kernels++;
@@ -791,6 +825,23 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   // grids, shared memory, partial offsets
   const int64_t ntiles = int64_t(1) << (nloc - L.k);
+  // lane-group inner-product accumulators: combine 2^shift lanes so that the
+  // shared accumulators stay within 24 KB (two 128-thread CTAs with 64 KB of
+  // transpose tiles still fit an SM; no per-op full warp reductions)
+  auto set_thread_acc = [](Launch& l) {
+    l.d.thread_acc = l.nb == 2 && l.d.nslots > 0;
+    l.d.acc_shift = 0;
+    while (l.d.acc_shift < 5 && size_t(l.d.nslots) * (l.threads >> l.d.acc_shift) * sizeof(double) > (24u << 10))
+      ++l.d.acc_shift;
+  };
+  auto memo_occ = [&](int kind, int R, int threads, size_t smem, auto query) {
+    const auto key = std::make_tuple(kind, R, threads, smem);
+    auto it = e->occ_memo.find(key);
+    if (it != e->occ_memo.end()) return it->second;
+    const int v = query();
+    e->occ_memo[key] = v;
+    return v;
+  };
   auto clamp_grid = [&](int per_sm) {
     const int64_t slots = int64_t(e->sms) * per_sm;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, slots)));
@@ -799,33 +850,36 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     switch (l.kind) {
       case L_SMEM_FWD:
         l.smem = fwd_smem(L.k, l.d.b);
-        l.grid = clamp_grid(occupancy(0, l.smem));
+        l.grid = clamp_grid(memo_occ(-1, 0, 0, l.smem, [&] { return occupancy(0, l.smem); }));
         break;
       case L_SMEM_REV:
         l.smem = rev_smem(L.k, l.d.b, l.d.nslots);
-        l.grid = clamp_grid(occupancy(2, l.smem));
+        l.grid = clamp_grid(memo_occ(-2, 0, 0, l.smem, [&] { return occupancy(2, l.smem); }));
         break;
       case L_REG:
         // per-thread inner-product accumulators when they fit a modest budget
-        l.d.thread_acc = l.nb == 2 && size_t(l.d.nslots) * l.threads * sizeof(double) <= (48u << 10);
+        set_thread_acc(l);
         if (l.jit) {
           l.smem = l.jit->smem;
-          int blocks = 0;
-          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, reinterpret_cast<const void*>(l.jit->fn),
-                                                            l.threads, l.smem) != cudaSuccess || blocks < 1) {
-            (void)cudaGetLastError();
-            blocks = 1;
+          if (l.jit->blocks_per_sm <= 0) {
+            int blocks = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, reinterpret_cast<const void*>(l.jit->fn),
+                                                              l.threads, l.smem) != cudaSuccess || blocks < 1) {
+              (void)cudaGetLastError();
+              blocks = 1;
+            }
+            l.jit->blocks_per_sm = blocks;
           }
-          l.grid = clamp_grid(blocks);
+          l.grid = clamp_grid(l.jit->blocks_per_sm);
           break;
         }
         l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin,
-                          l.d.seg_end - l.d.seg_begin, l.tiles, l.d.thread_acc != 0);
-        l.grid = clamp_grid(reg_occupancy(l.nb, l.R, l.threads, l.smem));
+                          l.d.seg_end - l.d.seg_begin, l.tiles, l.d.thread_acc != 0, l.d.acc_shift);
+        l.grid = clamp_grid(memo_occ(l.nb, l.R, l.threads, l.smem, [&] { return reg_occupancy(l.nb, l.R, l.threads, l.smem); }));
         break;
       case L_OBS:
-        l.smem = obs_smem(L.k, l.d.b);
-        l.grid = clamp_grid(occupancy(1, l.smem));
+        l.smem = obs_smem(L.k, l.d.b, l.d.op_end - l.d.op_begin);
+        l.grid = clamp_grid(memo_occ(-3, 0, 0, l.smem, [&] { return occupancy(1, l.smem); }));
         break;
       case L_OBS_DIRECT:
         l.smem = 0;
@@ -847,7 +901,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     std::vector<JitPass> passes;
     passes.reserve(regl.size());
     for (Launch* l : regl) {
-      l->d.thread_acc = l->nb == 2 && size_t(l->d.nslots) * l->threads * sizeof(double) <= (48u << 10);
+      set_thread_acc(*l);
       JitPass jp;
       jp.R = l->R;
       jp.nb = l->nb;
@@ -856,6 +910,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       jp.threads = l->threads;
       jp.nslots = l->d.nslots;
       jp.thread_acc = l->d.thread_acc != 0;
+      jp.acc_shift = l->d.acc_shift;
       jp.tiles = l->tiles;
       jp.stage = e->opt_stage != 0;
       jp.min_blocks = static_cast<int>(l->nb == 2 ? e->opt_jit_blocks_rev : e->opt_jit_blocks_fwd);

@@ -29,6 +29,7 @@ struct JitPass {
   int R = 4, nb = 1, k = 0, nloc = 0, threads = 0;
   int nslots = 0;
   bool thread_acc = false, tiles = false;
+  int acc_shift = 0;                 // thread_acc: lanes combined per accumulator (log2)
   bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
   int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
@@ -52,6 +53,7 @@ struct JitKernel {
   std::vector<CoefRef> coefs;      // fill order of the parameter block's c[]
   std::vector<int> dop_segs;       // shared-memory segments whose DevOp base is a parameter
   uint64_t device_mask = 0;        // devices whose kernel attributes are set
+  int blocks_per_sm = 0;           // occupancy (same for every B200), 0 = not queried yet
 };
 
 struct JitProgram {

@@ -58,30 +58,50 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
                                                        const DevTerm* __restrict__ terms,
                                                        double2* __restrict__ partials) {
   // src_state: the shard whose amplitudes feed this pass's terms (== psi unless the
-  // terms flip rank bits, d.xglob != 0: then the partner shard, fetched or peer-mapped)
+  // terms flip rank bits, d.xglob != 0: then the partner shard, fetched or peer-mapped).
+  // The host sorts a pass's terms by tile flip mask: terms sharing a flip share
+  // the partner amplitude, their signed coefficients are summed first.
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << d.k;
+  const int nt = d.op_end - d.op_begin;
   const bool remote = d.xglob != 0;
   double2* tile = reinterpret_cast<double2*>(smem_raw);
   double2* wsum = tile + N;
-  uint64_t* hi = reinterpret_cast<uint64_t*>(wsum + kWarps);
+  double2* cz = wsum + kWarps;                                   // [nt] coefficients, tile-uniform sign folded
+  uint32_t* txl = reinterpret_cast<uint32_t*>(cz + nt);          // [nt] flip masks
+  const int ne = (nt + 1) & ~1;                                  // keeps hi[] 8-byte aligned
+  uint32_t* tzl = txl + ne;                                      // [nt] tile sign masks
+  uint64_t* hi = reinterpret_cast<uint64_t*>(tzl + ne);
   build_hi(hi, d);
-  __syncthreads();
+  for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+    txl[j] = terms[d.op_begin + j].xl;
+    tzl[j] = terms[d.op_begin + j].zl;
+  }
   double2 e = make_double2(0.0, 0.0);
   const uint64_t ntiles = 1ull << (d.n - d.k);
   for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
     const uint64_t base = pdep64(T, d.rest);
     const uint64_t sbase = base | d.rank_bits;  // physical index bits for Z-signs / controls
     const uint64_t src_bits = sbase ^ d.xglob;  // non-tile bits of the source amplitude index
+    __syncthreads();  // previous tile done with tile[] / cz[]
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+      const DevTerm tm = terms[d.op_begin + j];
+      cz[j] = cneg_if(tm.c, par64(src_bits & tm.zo));
+    }
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) tile[t] = src_state[gidx(base, t, hi, d.b)];
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
       double2 acc = make_double2(0.0, 0.0);
-      for (int j = d.op_begin; j < d.op_end; ++j) {
-        const DevTerm tm = terms[j];
-        const uint32_t src = t ^ tm.xl;
-        const int sg = par32(src & tm.zl) ^ par64(src_bits & tm.zo);
-        acc = cfma(cneg_if(tm.c, sg), tile[src], acc);
+      for (int j = 0; j < nt;) {
+        const uint32_t xl = txl[j];
+        const uint32_t src = t ^ xl;
+        double2 cs = make_double2(0.0, 0.0);
+        do {
+          const double2 c = cneg_if(cz[j], par32(src & tzl[j]));
+          cs = make_double2(cs.x + c.x, cs.y + c.y);
+          ++j;
+        } while (j < nt && txl[j] == xl);
+        acc = cfma(cs, tile[src], acc);
       }
       const uint64_t m = gidx(base, t, hi, d.b);
       if (d.accumulate) {
@@ -92,9 +112,9 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
       }
       e = cjfma(remote ? psi[m] : tile[t], acc, e);
     }
-    __syncthreads();
   }
   e = warp_sum(e);
+  __syncthreads();
   if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = e;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -252,8 +272,9 @@ __global__ void k_half_pack(const double2* __restrict__ shard, double2* __restri
 // ------------------------------------------------------------ launchers --
 
 size_t fwd_smem(int k, int b) { return (sizeof(double2) << k) + (sizeof(uint64_t) << (k - b)); }
-size_t obs_smem(int k, int b) {
-  return (sizeof(double2) << k) + sizeof(double2) * kWarps + (sizeof(uint64_t) << (k - b));
+size_t obs_smem(int k, int b, int nterms) {
+  return (sizeof(double2) << k) + sizeof(double2) * kWarps + sizeof(double2) * nterms +
+         sizeof(uint32_t) * 2 * ((nterms + 1) & ~1) + (sizeof(uint64_t) << (k - b));
 }
 size_t rev_smem(int k, int b, int nslots) {
   return (2 * sizeof(double2) << k) + sizeof(double2) * kWarps * nslots + (sizeof(uint64_t) << (k - b));

@@ -9,7 +9,7 @@
 namespace svgb {
 
 size_t fwd_smem(int k, int b);
-size_t obs_smem(int k, int b);
+size_t obs_smem(int k, int b, int nterms);
 size_t rev_smem(int k, int b, int nslots);
 cudaError_t prepare_kernels(size_t max_smem);
 int occupancy(int which /*0 fwd, 1 obs, 2 rev*/, size_t smem);
@@ -34,7 +34,8 @@ void launch_finalize(const double2* partials, const SumSpec* specs, int count, d
 void launch_set_basis(double2* psi, uint64_t idx, cudaStream_t s);
 
 // register-tile passes (kernels_reg.cu)
-size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, int nsegs, bool tiles, bool thread_acc);
+size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, int nsegs, bool tiles, bool thread_acc,
+                int acc_shift);
 cudaError_t prepare_reg_kernels(size_t max_smem);
 int reg_occupancy(int nb, int R, int threads, size_t smem);
 int reg_max_threads(int R);

@@ -106,12 +106,13 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   SegDesc* ssegs = reinterpret_cast<SegDesc*>(wacc + nwarps * d.nslots);  // this pass's segments
   RegOp* sops = reinterpret_cast<RegOp*>(ssegs + nsegs);                  // this pass's register ops
   const int nops = d.op_end - d.op_begin;
-  double* tacc = d.thread_acc ? reinterpret_cast<double*>(sops + nops) : nullptr;  // [nslots][nthr]
-  double2* st0 = reinterpret_cast<double2*>(sops + nops) + (d.thread_acc ? (d.nslots * nthr + 1) / 2 : 0);
+  const int nacc = nthr >> d.acc_shift;  // accumulators per slot
+  double* tacc = d.thread_acc ? reinterpret_cast<double*>(sops + nops) : nullptr;  // [nslots][nacc]
+  double2* st0 = reinterpret_cast<double2*>(sops + nops) + (d.thread_acc ? (d.nslots * nacc + 1) / 2 : 0);
   double2* st1 = st0 + (1u << d.k);  // shared tiles (multi-segment passes)
   for (int i = threadIdx.x; i < nwarps * d.nslots; i += nthr) wacc[i] = make_double2(0.0, 0.0);
   if (tacc)
-    for (int i = threadIdx.x; i < d.nslots * nthr; i += nthr) tacc[i] = 0.0;
+    for (int i = threadIdx.x; i < d.nslots * nacc; i += nthr) tacc[i] = 0.0;
   {
     const uint4* src = reinterpret_cast<const uint4*>(rops + d.op_begin);
     uint4* dst = reinterpret_cast<uint4*>(sops);
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   }
   if (threadIdx.x < kMaxQubits) sq[threadIdx.x] = d.q[threadIdx.x];
   __syncthreads();
-  const IpSink sink{tacc, wacc, nthr, d.nslots, warp, lane};
+  const IpSink sink{tacc, wacc, nthr, d.nslots, warp, lane, d.acc_shift};
 
   const uint32_t tbase = uint32_t(lane) | (uint32_t(warp) << (5 + R));
   double2 v[NR], l[NR];
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
       acc = make_double2(acc.x + val.x, acc.y + val.y);
     }
     if (tacc)
-      for (int t = 0; t < nthr; ++t) acc.x += tacc[s * nthr + t];
+      for (int t = 0; t < nacc; ++t) acc.x += tacc[s * nacc + t];
     partials[d.part_off + static_cast<int64_t>(s) * gridDim.x + blockIdx.x] = acc;
   }
 }
@@ -260,8 +261,9 @@ cudaError_t allow_dynamic_smem(const void* fn, size_t max_smem) {
 }
 }  // namespace
 
-size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, int nsegs, bool tiles, bool thread_acc) {
-  const size_t tacc = thread_acc ? sizeof(double2) * ((size_t(nslots) * nwarps * 32 + 1) / 2) : 0;
+size_t reg_smem(int k, int nb, int nwarps, int nslots, int nops, int nsegs, bool tiles, bool thread_acc,
+                int acc_shift) {
+  const size_t tacc = thread_acc ? sizeof(double2) * ((size_t(nslots) * (nwarps * 32 >> acc_shift) + 1) / 2) : 0;
   return sizeof(double2) * (size_t(nwarps) * nslots + (tiles ? (size_t(nb) << k) : 0)) + sizeof(SegDesc) * nsegs +
          sizeof(RegOp) * nops + tacc;
 }

@@ -204,9 +204,10 @@ __device__ __forceinline__ void reg_op(double2 (&v)[1 << R], double2 (&l)[1 << R
 
 // Where a reverse op's inner product goes.
 struct IpSink {
-  double* tacc;   // per-thread accumulators [nslots][nthr] (or null)
+  double* tacc;   // lane-group accumulators [nslots][nthr >> shift] (or null)
   double2* wacc;  // per-warp accumulators [nwarps][nslots]
   int nthr, nslots, warp, lane;
+  int shift;      // lanes 2^shift apart are combined (butterfly) before the shared accumulate
 };
 
 __device__ __forceinline__ double warp_sum1(double v) {
@@ -254,7 +255,10 @@ __device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << 
     const double qs = (q[0] + q[1]) + (q[2] + q[3]);
     const double qk = kr * (slw ? -qs : qs);
     if (sink.tacc) {
-      sink.tacc[slot * sink.nthr + threadIdx.x] += qk;
+      double qa = qk;
+      for (int o = 1; o < (1 << sink.shift); o <<= 1) qa += __shfl_xor_sync(kFull, qa, o);
+      if ((sink.lane & ((1 << sink.shift) - 1)) == 0)
+        sink.tacc[slot * (sink.nthr >> sink.shift) + (threadIdx.x >> sink.shift)] += qa;
     } else {
       const double w = warp_sum1(qk);
       if (sink.lane == 0) sink.wacc[sink.warp * sink.nslots + slot].x += w;
