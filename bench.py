@@ -79,11 +79,11 @@ def _peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def _traffic_per_launch():
-    """ncu dram bytes per k_rev_pass launch, if a capture summary is committed."""
+def _traffic_per_launch(workload: str):
+    """ncu DRAM bytes per reverse-pass launch for this workload, from the committed capture summary."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_rev_pass.json")) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
+            return float(json.load(f)[workload]["dram_bytes_per_launch"])
     except Exception:
         return None
 
@@ -299,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = _peak()
     avg_launch_ms = rev_ms / max(1, rev_launches)
     achieved = 4 * S_rank / (avg_launch_ms * 1e-3) / 1e9
-    traffic = _traffic_per_launch()
+    traffic = _traffic_per_launch(f"cfg{args.config}") if args.qubits is None and world == 1 else None
     value = jobs * args.steps / (total_ms * 1e-3)
     B_alg = 6 * w.num_gates * S  # gate-level algorithmic bytes per gradient
     cpu = None
@@ -322,7 +322,8 @@ def run_ours(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "k_rev_pass", "bytes_per_launch": 4 * S_rank,
+            "traffic": traffic, "kernel": "reverse register-tile pass (generated svgb_jit; interpreter k_pass_reg<4,2>)",
+            "bytes_per_launch": 4 * S_rank,
             "avg_launch_ms": avg_launch_ms, "peak_source": peak_src,
         },
         "phase_ms": {k: round(v, 4) for k, v in phases.items()},
