@@ -76,6 +76,9 @@ def _account(counters, audit, num_gates: int, num_derivs: int) -> None:
     counters.clones += num_derivs + 2
     counters.inner_products += num_derivs
     counters.observable_applies += 1
+    if type(audit) is LiveStateAudit:  # the sequence below in closed form (O(1) per call)
+        audit.peak = max(audit.peak, audit.live + (4 if num_derivs else 3))
+        return
     audit.acquire()  # borrowed input
     audit.acquire()  # bra (psi, then lambda)
     audit.acquire()  # ket (phi)

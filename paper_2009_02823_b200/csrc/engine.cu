@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <deque>
 #include <map>
 #include <unordered_map>
 #include <tuple>
@@ -522,6 +523,24 @@ std::vector<Segment> memo_segments(const svg_engine* e, const std::vector<uint32
   return segs;
 }
 
+// The gates of one pass step (pointers into the problem or into remapped copies).
+struct GateList {
+  std::vector<const svg_gate*> ptr;
+  const svg_gate& operator[](size_t i) const { return *ptr[i]; }
+  size_t size() const { return ptr.size(); }
+  struct It {
+    const svg_gate* const* p;
+    const svg_gate& operator*() const { return **p; }
+    It& operator++() {
+      ++p;
+      return *this;
+    }
+    bool operator!=(const It& o) const { return p != o.p; }
+  };
+  It begin() const { return It{ptr.data()}; }
+  It end() const { return It{ptr.data() + ptr.size()}; }
+};
+
 // Physical copy of a gate under the logical -> physical qubit map of its step.
 svg_gate physical_gate(const svg_gate& g, const std::vector<int>& l2p) {
   svg_gate q = g;
@@ -532,7 +551,18 @@ svg_gate physical_gate(const svg_gate& g, const std::vector<int>& l2p) {
   return q;
 }
 
+// Host-side phase timing of lower() (svg_debug_lower_timing).
+thread_local double g_phase_ms[9];
+thread_local std::chrono::steady_clock::time_point g_phase_t;
+#define SVGB_PHASE(i)                                                                                  \
+  do {                                                                                                 \
+    const auto now_ = std::chrono::steady_clock::now();                                              \
+    g_phase_ms[(i)-1] += std::chrono::duration<double, std::milli>(now_ - g_phase_t).count();        \
+    g_phase_t = now_;                                                                                  \
+  } while (0)
+
 Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
+  g_phase_t = std::chrono::steady_clock::now();
   Lowered L;
   const int n = p->num_qubits;
   const int g = e->shard_bits;  // log2(shards): top g physical qubits select the shard
@@ -565,21 +595,31 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   std::vector<int> l2p_final;
   const std::vector<Step> steps = plan_schedule(logical, n, g, pp, &l2p_final);
   // physical gates per pass step, parallel to the step's items
-  std::vector<std::vector<svg_gate>> pgates(steps.size());
+  std::vector<GateList> pgates(steps.size());
+  std::deque<svg_gate> pstore;  // remapped copies (only when the qubit map is not the identity)
   std::vector<std::vector<GateShape>> pshapes(steps.size());
   for (size_t si = 0; si < steps.size(); ++si) {
     if (steps[si].swap) continue;
     for (int gi : steps[si].pass.items) {
-      pgates[si].push_back(physical_gate(p->gates[gi], steps[si].l2p));
-      pshapes[si].push_back(gate_shape(pgates[si].back()));
+      bool ident = true;
+      for (size_t q = 0; q < steps[si].l2p.size() && ident; ++q) ident = steps[si].l2p[q] == static_cast<int>(q);
+      if (ident) {
+        pgates[si].ptr.push_back(&p->gates[gi]);
+      } else {
+        pstore.push_back(physical_gate(p->gates[gi], steps[si].l2p));
+        pgates[si].ptr.push_back(&pstore.back());
+      }
+      pshapes[si].push_back(gate_shape(pgates[si][pgates[si].size() - 1]));
     }
   }
 
   std::vector<int> first_deriv(p->num_gates + 1, 0);
   for (int i = 0; i < p->num_gates; ++i) first_deriv[i + 1] = first_deriv[i] + p->gates[i].nderiv;
+  SVGB_PHASE(1);
   std::vector<Gen> gens(p->num_derivs);
   for (int d = 0; d < p->num_derivs; ++d) gens[d] = make_gen(p->gates[p->derivs[d].gate], p->derivs[d]);
 
+  SVGB_PHASE(2);
   // segments per pass (register path)
   std::vector<std::vector<Segment>> psegs(steps.size()), psegs_f(steps.size());
   if (L.reg) {
@@ -619,6 +659,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // default register layout for shared-memory segments: lowest non-lane positions
   auto default_regs = [](int R) { return ((1u << (5 + R)) - 1u) & ~31u; };
 
+  SVGB_PHASE(3);
   // forward schedule
   for (size_t si = 0; si < steps.size(); ++si) {
     if (steps[si].swap) {
@@ -627,7 +668,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       continue;
     }
     const Pass& ps = steps[si].pass;
-    const std::vector<svg_gate>& gs = pgates[si];
+    const GateList& gs = pgates[si];
     const TileMap tm = tile_map(ps.qmask);
     if (!L.reg) {
       Launch l;
@@ -668,6 +709,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     L.pass_bytes += 2 * S;
   }
 
+  SVGB_PHASE(4);
   // observable passes: terms in the final physical layout, grouped by the flip
   // pattern on rank bits (a nonzero pattern reads the partner shard's psi), then
   // by local flip mask into tiles
@@ -743,6 +785,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     }
   }
 
+  SVGB_PHASE(5);
   // reverse schedule: steps backwards (swaps undo themselves on phi and lambda),
   // gates backwards inside each pass
   std::vector<std::pair<int, int>> deriv_slot(p->num_derivs, {-1, -1});  // (rev launch, slot)
@@ -763,7 +806,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         continue;
       }
       const Pass& ps = steps[si].pass;
-      const std::vector<svg_gate>& gs = pgates[si];
+      const GateList& gs = pgates[si];
       const TileMap tm = tile_map(ps.qmask);
       uint32_t slot = 0;
       if (!L.reg) {
@@ -823,6 +866,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     }
   }
 
+  SVGB_PHASE(6);
   // grids, shared memory, partial offsets
   const int64_t ntiles = int64_t(1) << (nloc - L.k);
   // lane-group inner-product accumulators: combine 2^shift lanes so that the
@@ -891,6 +935,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     }
     if (l.smem > e->max_smem) throw InvalidArg("pass needs more shared memory than the device offers");
   };
+  SVGB_PHASE(7);
   // circuit-specialised kernels for the register-tile passes
   const bool want_jit = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits));
   if (want_jit) {
@@ -958,6 +1003,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   }
   L.sums.back() = SumSpec{energy_off, energy_count};
   for (const Step& st : steps) L.swaps += st.swap;
+  SVGB_PHASE(8);
   return L;
 }
 
@@ -1479,6 +1525,26 @@ int svg_plan_schedule(const svg_problem* p, int shards, int tile_qubits, int sms
     if (step_start_out) step_start_out[steps.size()] = pos;
     if (nsteps_out) *nsteps_out = static_cast<int32_t>(steps.size());
     if (tile_qubits_out) *tile_qubits_out = pp.k;
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_EINVAL, ex.what());
+  }
+}
+
+// Debug / profiling (not in the public header): host-only lowering of `p`
+// `reps` times on a device-less engine (interpreted kernels, no CUDA calls
+// that matter); out_ms[0..7] = accumulated per-phase milliseconds.
+extern "C" int svg_debug_lower_timing(const svg_problem* p, int reps, double* out_ms) {
+  try {
+    validate(p);
+    svg_engine e;
+    e.sms = 148;
+    e.max_smem = 232448;
+    e.opt_jit = 0;
+    for (double& v : g_phase_ms) v = 0.0;
+    for (int r = 0; r < reps; ++r) (void)lower(&e, p, true);
+    for (int i = 0; i < 8; ++i) out_ms[i] = g_phase_ms[i];
+    (void)cudaGetLastError();
     return SVG_OK;
   } catch (const std::exception& ex) {
     return fail(SVG_EINVAL, ex.what());

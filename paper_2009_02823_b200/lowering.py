@@ -25,6 +25,7 @@ so a VQE loop re-binds only the coefficient arrays.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -70,6 +71,7 @@ class Structure:
 
 
 _cache: dict[int, tuple] = {}
+_tls = threading.local()
 
 
 def _structure(circuit) -> Structure:
@@ -146,8 +148,15 @@ def _put(block: np.ndarray, m: np.ndarray) -> None:
 def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     """Gate and derivative tables for one theta (raises NonInvertibleGateError)."""
     st = _structure(circuit)
-    gates = st.gates.copy()
-    derivs = st.derivs.copy()
+    # per-thread working tables, reused across calls (every theta-dependent field
+    # is rewritten below; the rest is structure): no 100s-of-KB copy per call
+    tls = _tls.__dict__.setdefault("tables", {})
+    hit = tls.get(id(st))
+    if hit is None or hit[0] is not st:
+        if len(tls) > 16:
+            tls.clear()
+        hit = tls[id(st)] = (st, st.gates.copy(), st.derivs.copy())
+    gates, derivs = hit[1], hit[2]
     scale = derivative_scale()
     if st.rot_gates.size:
         ang = st.rot_alpha * params[st.rot_refs]
