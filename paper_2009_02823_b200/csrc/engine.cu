@@ -922,6 +922,20 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         l.grid = clamp_grid(memo_occ(l.nb, l.R, l.threads, l.smem, [&] { return reg_occupancy(l.nb, l.R, l.threads, l.smem); }));
         break;
       case L_OBS:
+        if (l.jit) {
+          l.smem = l.jit->smem;
+          if (l.jit->blocks_per_sm <= 0) {
+            int blocks = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, reinterpret_cast<const void*>(l.jit->fn),
+                                                              kThreads, l.smem) != cudaSuccess || blocks < 1) {
+              (void)cudaGetLastError();
+              blocks = 1;
+            }
+            l.jit->blocks_per_sm = blocks;
+          }
+          l.grid = clamp_grid(l.jit->blocks_per_sm);
+          break;
+        }
         l.smem = obs_smem(L.k, l.d.b, l.d.op_end - l.d.op_begin);
         l.grid = clamp_grid(memo_occ(-3, 0, 0, l.smem, [&] { return occupancy(1, l.smem); }));
         break;
@@ -972,6 +986,27 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       if (!jit_available(&why)) throw std::runtime_error(why);
       std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->device);
       for (size_t i = 0; i < regl.size(); ++i) regl[i]->jit = ks[i];
+      // observable passes (tiled)
+      std::vector<Launch*> obsl;
+      std::vector<JitObsPass> opasses;
+      for (Launch& l : L.obs) {
+        if (l.kind != L_OBS) continue;
+        JitObsPass op;
+        op.k = L.k;
+        op.b = l.d.b;
+        op.nloc = nloc;
+        op.threads = kThreads;
+        op.rest = l.d.rest;
+        op.q = l.d.q;
+        op.terms = L.terms.data() + l.d.op_begin;
+        op.nterms = l.d.op_end - l.d.op_begin;
+        op.accumulate = l.d.accumulate != 0;
+        op.remote = l.d.xglob != 0;
+        obsl.push_back(&l);
+        opasses.push_back(op);
+      }
+      std::vector<std::shared_ptr<JitKernel>> ko = jit_get_obs(opasses, e->device);
+      for (size_t i = 0; i < obsl.size(); ++i) obsl[i]->jit = ko[i];
     } catch (const std::exception& ex) {
       if (e->opt_jit == 2) throw;
       e->jit_error = ex.what();  // auto: keep the interpreted kernels
@@ -1207,10 +1242,18 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
           CK(cudaMemcpyAsync(scratch, src, shard_amps * sizeof(double2), cudaMemcpyDeviceToDevice, s));
           src = scratch;
         }
-        if (l.kind == L_OBS_DIRECT)
+        if (l.kind == L_OBS_DIRECT) {
           launch_obs_direct(d, l.grid, s, v.psi, src, v.lam, dterms, v.part);
-        else
+        } else if (l.jit) {
+          const JitObsArgsHead head{v.psi, src, v.lam, v.part, d.part_off, d.rank_bits, d.xglob};
+          std::vector<unsigned char> args = jit_obs_args(*l.jit, head, L.terms.data() + d.op_begin);
+          void* params[] = {args.data()};
+          CK(cudaLaunchKernel(reinterpret_cast<const void*>(l.jit->fn), dim3(l.grid), dim3(kThreads), params, l.smem,
+                              s));
+          ++jit_launches;
+        } else {
           launch_obs(d, l.grid, l.smem, s, v.psi, src, v.lam, dterms, v.part);
+        }
         ++launches;
       }
     }

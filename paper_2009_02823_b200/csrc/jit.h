@@ -40,9 +40,19 @@ struct JitPass {
   int op_begin = 0;
 };
 
+// One tiled observable pass (k_obs_pass's work) for the generator.
+struct JitObsPass {
+  int k = 0, b = 0, nloc = 0, threads = 256;
+  uint64_t rest = 0;
+  const uint8_t* q = nullptr;
+  const DevTerm* terms = nullptr;  // sorted by tile flip mask
+  int nterms = 0;
+  bool accumulate = false, remote = false;
+};
+
 // Where parameter c[i] comes from, relative to the pass.
 struct CoefRef {
-  enum Kind : uint8_t { A, BB, KR, KAX, KAY, KBX, KBY, SCALE } kind;
+  enum Kind : uint8_t { A, BB, KR, KAX, KAY, KBX, KBY, SCALE, TRE, TIM } kind;
   int index;  // register op (relative to op_begin) or segment (relative to seg_begin)
 };
 
@@ -74,7 +84,20 @@ struct JitArgsHead {
   uint64_t rank_bits;
 };
 
+// Parameter block of a generated observable pass (then double c[]).
+struct JitObsArgsHead {
+  const double2* psi;
+  const double2* src;
+  double2* lam;
+  double2* partials;
+  int64_t part_off;
+  uint64_t rank_bits;
+  uint64_t xglob;
+};
+
 bool jit_available(std::string* why);
+std::vector<std::shared_ptr<JitKernel>> jit_get_obs(const std::vector<JitObsPass>& passes, int device);
+std::vector<unsigned char> jit_obs_args(const JitKernel& kern, const JitObsArgsHead& head, const DevTerm* terms);
 JitProgram jit_generate(const JitPass& p);
 // Kernels for the passes: cache hits by structural key; misses are generated
 // and compiled (in parallel), then cached.  Throws std::runtime_error on compile / load failure.

@@ -225,16 +225,7 @@ __global__ void __launch_bounds__(R == 3 ? kRegThreads : kRegThreads / 2, R == 3
   }
   if (d.nslots == 0) return;
   __syncthreads();
-  for (int s = threadIdx.x; s < d.nslots; s += nthr) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int w = 0; w < nwarps; ++w) {
-      const double2 val = wacc[w * d.nslots + s];
-      acc = make_double2(acc.x + val.x, acc.y + val.y);
-    }
-    if (tacc)
-      for (int t = 0; t < nacc; ++t) acc.x += tacc[s * nacc + t];
-    partials[d.part_off + static_cast<int64_t>(s) * gridDim.x + blockIdx.x] = acc;
-  }
+  flush_partials(wacc, tacc, d.nslots, nwarps, nacc, partials + d.part_off, warp, lane);
 }
 
 #define SVGB_INST(R, NB)                                                                                   \

@@ -276,6 +276,25 @@ __device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << 
 }
 
 
+// Per-CTA slot sums -> partials[s * gridDim.x + blockIdx.x]: one warp per slot,
+// lanes stride over the per-warp and lane-group accumulators, then a butterfly
+// (fixed order: deterministic).
+__device__ __forceinline__ void flush_partials(const double2* wacc, const double* tacc, int nslots, int nwarps,
+                                               int nacc, double2* out, int warp, int lane) {
+  for (int s = warp; s < nslots; s += nwarps) {
+    double x = 0.0, y = 0.0;
+    for (int w = lane; w < nwarps; w += 32) {
+      x += wacc[w * nslots + s].x;
+      y += wacc[w * nslots + s].y;
+    }
+    if (tacc)
+      for (int t = lane; t < nacc; t += 32) x += tacc[s * nacc + t];
+    x = warp_sum1(x);
+    y = warp_sum1(y);
+    if (lane == 0) out[static_cast<long long>(s) * gridDim.x + blockIdx.x] = make_double2(x, y);
+  }
+}
+
 // ---- asynchronous tile staging (cp.async, 16 B per copy, L1 bypass) ----
 // Each thread stages its own 2^R amplitudes of the NEXT tile into a private
 // slice of shared memory ([j][thread] layout: conflict-free 16-byte rows) while
