@@ -162,7 +162,7 @@ struct svg_engine {
   size_t max_smem = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 4, opt_reg_bits_fwd = 4, opt_prefetch = 0;
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 0, opt_reg_bits_fwd = 0, opt_prefetch = 0;  // reg bits 0: auto
   // virtual engines: run the NCCL-mode data path (half-shard pack -> copy ->
   // unpack, partner fetch into scratch) with device copies as the transport
   int64_t opt_emulate_transport = 0;
@@ -574,8 +574,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   L.k = choose_tile_qubits(nloc, static_cast<int>(e->opt_tile), e->sms);
   L.b = (nloc <= L.k) ? nloc : std::min(5, L.k - 2);
   if (g > 0 && L.b < 5 && nloc > L.k) throw InvalidArg("sharded engines need >= 7 qubits per shard");
-  const int RB = static_cast<int>(e->opt_reg_bits);      // reverse passes
-  const int RF = static_cast<int>(e->opt_reg_bits_fwd);  // forward passes
+  // register bits (amplitudes per thread per buffer = 2^R): auto = 3 for shards of
+  // <= 23 qubits (more threads per tile: better latency hiding when a pass is only
+  // a few tile rounds), 4 above (fewer ops per amplitude; measured cfg 2 / cfg 3)
+  const int Rauto = nloc <= 23 ? 3 : 4;
+  const int RB = e->opt_reg_bits ? static_cast<int>(e->opt_reg_bits) : Rauto;          // reverse passes
+  const int RF = e->opt_reg_bits_fwd ? static_cast<int>(e->opt_reg_bits_fwd) : Rauto;  // forward passes
   L.R = RB;
   auto fits = [&](int R) { return L.k - 5 - R >= 0 && (32 << (L.k - 5 - R)) <= reg_max_threads(R); };
   L.reg = e->opt_kernel != 1 && L.b >= 5 && fits(RB) && fits(RF);
@@ -1502,8 +1506,7 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "profile") {
     e->opt_profile = value;
   } else if (k == "reg_bits" || k == "reg_bits_fwd") {
-    if (value == 0) value = 4;
-    if (value != 3 && value != 4) return fail(SVG_EINVAL, k + " must be 3 or 4");
+    if (value != 0 && value != 3 && value != 4) return fail(SVG_EINVAL, k + " must be 0 (auto), 3 or 4");
     (k == "reg_bits" ? e->opt_reg_bits : e->opt_reg_bits_fwd) = value;
   } else if (k == "prefetch") {  // accepted for compatibility; the bulk-copy tile prefetch was removed
     e->opt_prefetch = value != 0;

@@ -76,12 +76,13 @@ def _with_options(opts, fn):
 
 
 @pytest.mark.parametrize("name", ["cfg2_n12", "cfg3_n14", "cfg4_n16", "cfg5_n15", "cfg1"])
-@pytest.mark.parametrize("kernel", [1, 2])
-def test_both_kernel_families_match_golden(name, kernel):
-    """Shared-memory tiles (1) and register tiles (2) against the reference's outputs."""
+@pytest.mark.parametrize("kernel,reg_bits", [(1, 0), (2, 3), (2, 4)])
+def test_both_kernel_families_match_golden(name, kernel, reg_bits):
+    """Shared-memory tiles (1) and interpreted register tiles (2, R = 3 / 4) against the reference's outputs."""
     rec = GOLD[name]
     circ, theta, obs, inp, _ = materialize(SMALL[name])
-    rep = _with_options({"kernel": kernel}, lambda: sv.reverse_mode_gradient(circ, theta, obs, inp))
+    rep = _with_options({"kernel": kernel, "reg_bits": reg_bits, "reg_bits_fwd": reg_bits},
+                        lambda: sv.reverse_mode_gradient(circ, theta, obs, inp))
     assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
 
