@@ -170,6 +170,7 @@ struct svg_engine {
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
   int64_t opt_stage = 1;  // generated kernels: stage the next tile with cp.async
+  int64_t opt_pdl = 1;    // generated kernels: programmatic dependent launch
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   mutable std::string jit_error;
   // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
@@ -1183,6 +1184,23 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     };
 
     int jit_launches = 0;
+    // generated kernels go out with programmatic dependent launch (they call
+    // griddepcontrol.wait before their first global access)
+    auto launch_generated = [&](cudaKernel_t fn, int grid, int threads, size_t smem, cudaStream_t st,
+                                std::vector<unsigned char>& args) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = e->opt_pdl ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      void* params[] = {args.data()};
+      CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), params));
+    };
     // register-tile pass: the circuit-specialised kernel when there is one, else the interpreter
     auto launch_reg = [&](const Launch& l, const PassDesc& d, double2* b0, double2* b1, double2* prt) {
       if (!l.jit) {
@@ -1192,8 +1210,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       const JitArgsHead head{b0, b1, dops, dcoef, prt, d.part_off, d.rank_bits};
       std::vector<unsigned char> args =
           jit_args(*l.jit, head, L.segs.data() + d.seg_begin, L.rops.data() + d.op_begin);
-      void* params[] = {args.data()};
-      CK(cudaLaunchKernel(reinterpret_cast<const void*>(l.jit->fn), dim3(l.grid), dim3(l.threads), params, l.smem, s));
+      launch_generated(l.jit->fn, l.grid, l.threads, l.smem, s, args);
       ++jit_launches;
     };
     int64_t launches = 0, h2d = bl.total, d2h = 0;
@@ -1251,9 +1268,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         } else if (l.jit) {
           const JitObsArgsHead head{v.psi, src, v.lam, v.part, d.part_off, d.rank_bits, d.xglob};
           std::vector<unsigned char> args = jit_obs_args(*l.jit, head, L.terms.data() + d.op_begin);
-          void* params[] = {args.data()};
-          CK(cudaLaunchKernel(reinterpret_cast<const void*>(l.jit->fn), dim3(l.grid), dim3(kThreads), params, l.smem,
-                              s));
+          launch_generated(l.jit->fn, l.grid, kThreads, l.smem, s, args);
           ++jit_launches;
         } else {
           launch_obs(d, l.grid, l.smem, s, v.psi, src, v.lam, dterms, v.part);
@@ -1518,6 +1533,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "jit_blocks_fwd" || k == "jit_blocks_rev") {
     if (value < 0 || value > 8) return fail(SVG_EINVAL, k + " must be in [0, 8]");
     (k == "jit_blocks_fwd" ? e->opt_jit_blocks_fwd : e->opt_jit_blocks_rev) = value;
+  } else if (k == "pdl") {
+    e->opt_pdl = value != 0;
   } else if (k == "stage") {
     e->opt_stage = value != 0;
   } else if (k == "jit") {
