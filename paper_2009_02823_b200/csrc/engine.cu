@@ -176,7 +176,8 @@ struct svg_engine {
   // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
   mutable std::map<std::tuple<int, int, int, size_t>, int> occ_memo;
   // segment plans are pure functions of a pass's flip / touch / dense pattern
-  mutable std::unordered_map<std::string, std::vector<Segment>> seg_memo;  // why auto mode fell back to the interpreted kernels
+  mutable std::unordered_map<std::string, std::vector<Segment>> seg_memo;
+  mutable std::unordered_map<std::string, std::pair<std::vector<Step>, std::vector<int>>> plan_memo;  // why auto mode fell back to the interpreted kernels
   DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
   // sharding: the state is split over 2^shard_bits shards by its top physical
@@ -598,7 +599,27 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   std::vector<GateShape> logical(p->num_gates);
   for (int i = 0; i < p->num_gates; ++i) logical[i] = gate_shape(p->gates[i]);
   std::vector<int> l2p_final;
-  const std::vector<Step> steps = plan_schedule(logical, n, g, pp, &l2p_final);
+  std::vector<Step> steps;
+  {  // the schedule is a pure function of the gate shapes and plan parameters: memoised
+    std::string key;
+    key.reserve(32 + logical.size() * sizeof(GateShape));
+    const int32_t head[] = {n, g, pp.n, pp.k, pp.b, pp.max_items, pp.max_derivs};
+    key.append(reinterpret_cast<const char*>(head), sizeof(head));
+    for (const GateShape& sh : logical) {
+      key.append(reinterpret_cast<const char*>(&sh.flip), 8);
+      key.append(reinterpret_cast<const char*>(&sh.touch), 8);
+      key.append(reinterpret_cast<const char*>(&sh.nderiv), 4);
+    }
+    auto it = e->plan_memo.find(key);
+    if (it != e->plan_memo.end()) {
+      steps = it->second.first;
+      l2p_final = it->second.second;
+    } else {
+      steps = plan_schedule(logical, n, g, pp, &l2p_final);
+      if (e->plan_memo.size() > 64) e->plan_memo.clear();
+      e->plan_memo.emplace(std::move(key), std::make_pair(steps, l2p_final));
+    }
+  }
   // physical gates per pass step, parallel to the step's items
   std::vector<GateList> pgates(steps.size());
   std::deque<svg_gate> pstore;  // remapped copies (only when the qubit map is not the identity)
