@@ -1491,7 +1491,7 @@ int svg_engine_create_sharded(int device, int world, int rank, const uint8_t ncc
   e->shard_bits = g;
   e->shards_local = 1;
   e->rank = rank;
-  if (world > 1) {
+  {  // world 1 too: a one-rank communicator runs the same all-gather path
     try {
       NcclUniqueId id;
       std::memcpy(id.internal, nccl_id, sizeof(id.internal));

@@ -157,3 +157,17 @@ def test_nccl_data_path_emulated(name, shards):
     rep = _run(circ, theta, obs, inp, method, eng)
     assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg5_n15", "cfg3_n14", "nh_all_kinds_6"])
+def test_nccl_engine_single_rank(name):
+    """The NCCL engine on one GPU (one-rank communicator): NCCL loading, communicator
+    setup and the result all-gather run for real; exchanges need >= 2 ranks."""
+    from paper_2009_02823_b200 import _native
+
+    rec = GOLD[name]
+    circ, theta, obs, inp, method = materialize(SMALL[name])
+    eng = _native.Engine(0, shards=1, rank=0, nccl_id=_native.nccl_unique_id())
+    rep = _run(circ, theta, obs, inp, method, eng)
+    assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
