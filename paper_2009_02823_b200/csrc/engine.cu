@@ -171,6 +171,7 @@ struct svg_engine {
   int64_t opt_jit = 1;
   int64_t opt_stage = 1;  // generated kernels: stage the next tile with cp.async
   int64_t opt_pdl = 1;    // generated kernels: programmatic dependent launch
+  int64_t opt_fuse_diag = 1;  // generated reverse kernels: fused runs of diagonal rotations
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   mutable std::string jit_error;
   // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
@@ -998,6 +999,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       jp.acc_shift = l->d.acc_shift;
       jp.tiles = l->tiles;
       jp.stage = e->opt_stage != 0;
+      jp.fuse_diag = e->opt_fuse_diag != 0;
       jp.min_blocks = static_cast<int>(l->nb == 2 ? e->opt_jit_blocks_rev : e->opt_jit_blocks_fwd);
       jp.rest = l->d.rest;
       jp.q = l->d.q;
@@ -1554,6 +1556,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "jit_blocks_fwd" || k == "jit_blocks_rev") {
     if (value < 0 || value > 8) return fail(SVG_EINVAL, k + " must be in [0, 8]");
     (k == "jit_blocks_fwd" ? e->opt_jit_blocks_fwd : e->opt_jit_blocks_rev) = value;
+  } else if (k == "fuse_diag") {
+    e->opt_fuse_diag = value != 0;
   } else if (k == "pdl") {
     e->opt_pdl = value != 0;
   } else if (k == "stage") {

@@ -30,6 +30,7 @@ struct JitPass {
   int nslots = 0;
   bool thread_acc = false, tiles = false;
   int acc_shift = 0;                 // thread_acc: lanes combined per accumulator (log2)
+  bool fuse_diag = true;             // reverse passes: fuse runs of diagonal rotations
   bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
   int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
@@ -52,8 +53,9 @@ struct JitObsPass {
 
 // Where parameter c[i] comes from, relative to the pass.
 struct CoefRef {
-  enum Kind : uint8_t { A, BB, KR, KAX, KAY, KBX, KBY, SCALE, TRE, TIM } kind;
-  int index;  // register op (relative to op_begin) or segment (relative to seg_begin)
+  enum Kind : uint8_t { A, BB, KR, KAX, KAY, KBX, KBY, SCALE, TRE, TIM, KRRUN } kind;
+  int index;    // register op (relative to op_begin) or segment (relative to seg_begin)
+  int aux = 0;  // KRRUN: first op of the fused diagonal run (kr rescaled to the run's start)
 };
 
 struct JitKernel {

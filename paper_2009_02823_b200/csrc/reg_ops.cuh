@@ -222,6 +222,19 @@ __device__ __forceinline__ void scale_tile(double2 (&v)[1 << R], double s) {
   for (int j = 0; j < (1 << R); ++j) v[j] = make_double2(v[j].x * s, v[j].y * s);
 }
 
+// One real inner-product contribution of this thread into `slot`.
+__device__ __forceinline__ void sink_real(const IpSink& sink, uint32_t slot, double qk) {
+  if (sink.tacc) {
+    double qa = qk;
+    for (int o = 1; o < (1 << sink.shift); o <<= 1) qa += __shfl_xor_sync(kFull, qa, o);
+    if ((sink.lane & ((1 << sink.shift) - 1)) == 0)
+      sink.tacc[slot * (sink.nthr >> sink.shift) + (threadIdx.x >> sink.shift)] += qa;
+  } else {
+    const double w = warp_sum1(qk);
+    if (sink.lane == 0) sink.wacc[sink.warp * sink.nslots + slot].x += w;
+  }
+}
+
 // Kernel-local variant id (computed on the host, see engine.cu emit_rop):
 //   id = pattern + Pat<R>::N * (ctrl + 2 * mode)
 //   forward kernels (NB 1), kFwdModes: 0/1 rotation (BI 0/1), 2/3 signed permutation (BI 0/1)
@@ -253,16 +266,7 @@ __device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << 
   }
   if constexpr (IPK == 1) {  // per-thread accumulator: no per-op warp reduction
     const double qs = (q[0] + q[1]) + (q[2] + q[3]);
-    const double qk = kr * (slw ? -qs : qs);
-    if (sink.tacc) {
-      double qa = qk;
-      for (int o = 1; o < (1 << sink.shift); o <<= 1) qa += __shfl_xor_sync(kFull, qa, o);
-      if ((sink.lane & ((1 << sink.shift) - 1)) == 0)
-        sink.tacc[slot * (sink.nthr >> sink.shift) + (threadIdx.x >> sink.shift)] += qa;
-    } else {
-      const double w = warp_sum1(qk);
-      if (sink.lane == 0) sink.wacc[sink.warp * sink.nslots + slot].x += w;
-    }
+    sink_real(sink, slot, kr * (slw ? -qs : qs));
   } else if constexpr (IPK == 3) {
     if (slw) z = make_double2(-z.x, -z.y);
     z = warp_sum(z);
