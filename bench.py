@@ -65,6 +65,7 @@ def _args():
     ap.add_argument("--no-pdl", action="store_true", help="generated kernels: no programmatic dependent launch")
     ap.add_argument("--no-fuse-diag", action="store_true", help="generated kernels: no fused diagonal runs")
     ap.add_argument("--jit", type=int, default=1, help="circuit-specialised kernels: 0 off, 1 auto, 2 always")
+    ap.add_argument("--opt", action="append", default=[], help="extra engine option KEY=VALUE (repeatable)")
     ap.add_argument("--jit-blocks", type=str, default="0,0", help="generated kernels: min CTAs/SM fwd,rev (0 default)")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one state over the ranks (default for cfg 4/5)")
     ap.add_argument("--max-gates", type=int, default=0, help="gates per pass cap (0: planner default)")
@@ -228,6 +229,9 @@ def run_ours(args, rank, world, local_rank):
     jb = [int(x) for x in args.jit_blocks.split(",")]
     eng.set_option("jit_blocks_fwd", jb[0])
     eng.set_option("jit_blocks_rev", jb[1])
+    for kv in args.opt:
+        key, val = kv.split("=")
+        eng.set_option(key, int(val))
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

@@ -160,6 +160,7 @@ struct svg_engine {
   int device = 0;
   int sms = 148;
   size_t max_smem = 0;
+  size_t max_smem_sm = 233472;  // shared memory per SM (B200: 228 KB)
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 0, opt_reg_bits_fwd = 0, opt_prefetch = 0;  // reg bits 0: auto
@@ -172,8 +173,15 @@ struct svg_engine {
   int64_t opt_stage = 1;  // generated kernels: stage the next tile with cp.async
   int64_t opt_pdl = 1;    // generated kernels: programmatic dependent launch
   int64_t opt_fuse_diag = 1;  // generated reverse kernels: fused runs of diagonal rotations
+  int64_t opt_acc_prefetch = 1;  // generated reverse kernels: accumulator loads ahead of the op
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
+  // reverse passes: shared-memory budget (KB) of the lane-group inner-product
+  // accumulators; 0 = auto (interpreter 24 KB; generated kernels: whatever the
+  // CTA's share of the SM leaves next to its tile buffers)
+  int64_t opt_acc_kb = 0;
   mutable std::string jit_error;
+  bool jit_dry_run = false;        // svg_debug_jit_check
+  mutable int jit_dry_count = 0;
   // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
   mutable std::map<std::tuple<int, int, int, size_t>, int> occ_memo;
   // segment plans are pure functions of a pass's flip / touch / dense pattern
@@ -899,10 +907,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // lane-group inner-product accumulators: combine 2^shift lanes so that the
   // shared accumulators stay within 24 KB (two 128-thread CTAs with 64 KB of
   // transpose tiles still fit an SM; no per-op full warp reductions)
-  auto set_thread_acc = [](Launch& l) {
+  const size_t acc_budget = size_t(e->opt_acc_kb ? e->opt_acc_kb : 24) << 10;
+  auto set_thread_acc = [acc_budget](Launch& l) {
     l.d.thread_acc = l.nb == 2 && l.d.nslots > 0;
     l.d.acc_shift = 0;
-    while (l.d.acc_shift < 5 && size_t(l.d.nslots) * (l.threads >> l.d.acc_shift) * sizeof(double) > (24u << 10))
+    while (l.d.acc_shift < 5 && size_t(l.d.nslots) * (l.threads >> l.d.acc_shift) * sizeof(double) > acc_budget)
       ++l.d.acc_shift;
   };
   auto memo_occ = [&](int kind, int R, int threads, size_t smem, auto query) {
@@ -988,6 +997,20 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     passes.reserve(regl.size());
     for (Launch* l : regl) {
       set_thread_acc(*l);
+      if (l->d.thread_acc && e->opt_acc_kb == 0) {
+        // auto budget: the SM's shared memory split over the kernel's CTAs per SM,
+        // minus tile / staging buffers and per-warp accumulators.  Every halving
+        // of the accumulators costs a butterfly step per op (measured: 40-slot
+        // passes 8 % slower at shift 1 than at shift 0).
+        const int blocks = l->nb == 2 ? (e->opt_jit_blocks_rev ? int(e->opt_jit_blocks_rev) : 2)
+                                      : (e->opt_jit_blocks_fwd ? int(e->opt_jit_blocks_fwd) : (l->R == 3 ? 2 : 4));
+        const size_t share = std::min<size_t>(e->max_smem, (size_t(e->max_smem_sm) / blocks) - 1024);
+        const size_t fixed = (sizeof(double2) << L.k) * l->nb + sizeof(double2) * (l->threads / 32) * l->d.nslots;
+        const size_t budget = share > fixed + 4096 ? share - fixed : 4096;
+        l->d.acc_shift = 0;
+        while (l->d.acc_shift < 5 && size_t(l->d.nslots) * (l->threads >> l->d.acc_shift) * sizeof(double) > budget)
+          ++l->d.acc_shift;
+      }
       JitPass jp;
       jp.R = l->R;
       jp.nb = l->nb;
@@ -1000,6 +1023,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       jp.tiles = l->tiles;
       jp.stage = e->opt_stage != 0;
       jp.fuse_diag = e->opt_fuse_diag != 0;
+      jp.acc_prefetch = e->opt_acc_prefetch != 0;
       jp.min_blocks = static_cast<int>(l->nb == 2 ? e->opt_jit_blocks_rev : e->opt_jit_blocks_fwd);
       jp.rest = l->d.rest;
       jp.q = l->d.q;
@@ -1012,8 +1036,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     try {
       std::string why;
       if (!jit_available(&why)) throw std::runtime_error(why);
-      std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->device);
-      for (size_t i = 0; i < regl.size(); ++i) regl[i]->jit = ks[i];
+      std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->jit_dry_run ? -1 : e->device);
+      for (size_t i = 0; i < ks.size(); ++i) regl[i]->jit = ks[i];
       // observable passes (tiled)
       std::vector<Launch*> obsl;
       std::vector<JitObsPass> opasses;
@@ -1033,10 +1057,15 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         obsl.push_back(&l);
         opasses.push_back(op);
       }
-      std::vector<std::shared_ptr<JitKernel>> ko = jit_get_obs(opasses, e->device);
-      for (size_t i = 0; i < obsl.size(); ++i) obsl[i]->jit = ko[i];
+      std::vector<std::shared_ptr<JitKernel>> ko = jit_get_obs(opasses, e->jit_dry_run ? -1 : e->device);
+      for (size_t i = 0; i < ko.size(); ++i) obsl[i]->jit = ko[i];
+      if (e->jit_dry_run) {  // svg_debug_jit_check: sources generated and compiled; keep the interpreter
+        e->jit_dry_count += static_cast<int>(passes.size() + opasses.size());
+        throw std::runtime_error("dry run");
+      }
     } catch (const std::exception& ex) {
-      if (e->opt_jit == 2) throw;
+      if (e->jit_dry_run && std::string(ex.what()) != "dry run") throw;
+      if (e->opt_jit == 2 && !e->jit_dry_run) throw;
       e->jit_error = ex.what();  // auto: keep the interpreted kernels
     }
   }
@@ -1439,6 +1468,7 @@ int svg_engine_create(int device, svg_engine** out) {
                                           std::to_string(prop.major * 10 + prop.minor));
     e->sms = prop.multiProcessorCount;
     e->max_smem = prop.sharedMemPerBlockOptin;
+    e->max_smem_sm = prop.sharedMemPerMultiprocessor;
     CK(prepare_kernels(e->max_smem));
     CK(prepare_reg_kernels(e->max_smem));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
@@ -1556,6 +1586,11 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "jit_blocks_fwd" || k == "jit_blocks_rev") {
     if (value < 0 || value > 8) return fail(SVG_EINVAL, k + " must be in [0, 8]");
     (k == "jit_blocks_fwd" ? e->opt_jit_blocks_fwd : e->opt_jit_blocks_rev) = value;
+  } else if (k == "acc_kb") {
+    if (value < 0 || value > 200) return fail(SVG_EINVAL, "acc_kb must be in [0 (auto), 200]");
+    e->opt_acc_kb = value;
+  } else if (k == "acc_prefetch") {
+    e->opt_acc_prefetch = value != 0;
   } else if (k == "fuse_diag") {
     e->opt_fuse_diag = value != 0;
   } else if (k == "pdl") {
@@ -1613,6 +1648,34 @@ int svg_plan_schedule(const svg_problem* p, int shards, int tile_qubits, int sms
     if (step_start_out) step_start_out[steps.size()] = pos;
     if (nsteps_out) *nsteps_out = static_cast<int32_t>(steps.size());
     if (tile_qubits_out) *tile_qubits_out = pp.k;
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_EINVAL, ex.what());
+  }
+}
+
+// Debug / test hook (not in the public header): lower `p` on a device-less
+// engine with circuit-specialised kernels forced on, generate and NVRTC-compile
+// every distinct pass kernel (nothing is loaded).  opts: tile_qubits, reg_bits,
+// reg_bits_fwd, acc_kb (0: engine defaults).  *npasses = register passes covered.
+extern "C" int svg_debug_jit_check(const svg_problem* p, const int64_t* opts, int32_t* npasses) {
+  try {
+    validate(p);
+    svg_engine e;
+    e.sms = 148;
+    e.max_smem = 232448;
+    e.opt_jit = 2;
+    e.jit_dry_run = true;
+    if (opts) {
+      e.opt_tile = opts[0];
+      e.opt_reg_bits = opts[1];
+      e.opt_reg_bits_fwd = opts[2];
+      e.opt_acc_kb = opts[3];
+    }
+    (void)lower(&e, p, true);
+    (void)cudaGetLastError();
+    if (npasses) *npasses = e.jit_dry_count;
+    if (e.jit_error != "dry run") return fail(SVG_EINVAL, "generated kernels: " + e.jit_error);
     return SVG_OK;
   } catch (const std::exception& ex) {
     return fail(SVG_EINVAL, ex.what());

@@ -31,6 +31,7 @@ struct JitPass {
   bool thread_acc = false, tiles = false;
   int acc_shift = 0;                 // thread_acc: lanes combined per accumulator (log2)
   bool fuse_diag = true;             // reverse passes: fuse runs of diagonal rotations
+  bool acc_prefetch = true;          // reverse passes: load an op's accumulator before the op
   bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
   int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
@@ -103,6 +104,7 @@ std::vector<unsigned char> jit_obs_args(const JitKernel& kern, const JitObsArgsH
 JitProgram jit_generate(const JitPass& p);
 // Kernels for the passes: cache hits by structural key; misses are generated
 // and compiled (in parallel), then cached.  Throws std::runtime_error on compile / load failure.
+// device < 0: dry run -- generate and compile every distinct structure, load nothing, return {}.
 std::vector<std::shared_ptr<JitKernel>> jit_get(const std::vector<JitPass>& passes, int device);
 // Parameter block for one launch.
 std::vector<unsigned char> jit_args(const JitKernel& kern, const JitArgsHead& head, const SegDesc* segs,

@@ -243,10 +243,12 @@ __device__ __forceinline__ void sink_real(const IpSink& sink, uint32_t slot, dou
 // ctrl = 1 selects the unscaled form with control predicates (also used, with an
 // all-pass mask, for rotations whose a is too small to defer).
 constexpr int kFwdModes = 4, kRevModes = 5;
-template <int R, int NB, int V>
-__device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
-                                        uint32_t slw, bool rbi, uint32_t slot, double kr, double2 ka, double2 kb,
-                                        const IpSink& sink) {
+// RET: a single-component inner product is returned instead of accumulated
+// (the generated kernels add it to an accumulator they loaded before the op).
+template <int R, int NB, int V, bool RET = false>
+__device__ __forceinline__ double op_body(double2 (&v)[1 << R], double2 (&l)[1 << R], const OpCtx& c, uint32_t xl,
+                                          uint32_t slw, bool rbi, uint32_t slot, double kr, double2 ka, double2 kb,
+                                          const IpSink& sink) {
   constexpr int NP = Pat<R>::N;
   constexpr int P = V % NP;
   constexpr bool CTRL = (V / NP) % 2;
@@ -266,6 +268,7 @@ __device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << 
   }
   if constexpr (IPK == 1) {  // per-thread accumulator: no per-op warp reduction
     const double qs = (q[0] + q[1]) + (q[2] + q[3]);
+    if constexpr (RET) return kr * (slw ? -qs : qs);
     sink_real(sink, slot, kr * (slw ? -qs : qs));
   } else if constexpr (IPK == 3) {
     if (slw) z = make_double2(-z.x, -z.y);
@@ -277,6 +280,7 @@ __device__ __forceinline__ void op_body(double2 (&v)[1 << R], double2 (&l)[1 << 
       acc = make_double2(acc.x + contrib.x, acc.y + contrib.y);
     }
   }
+  return 0.0;
 }
 
 
@@ -324,10 +328,10 @@ __device__ __forceinline__ void unstage(double2 (&v)[1 << R], const double2* stg
 // One register op with its structure as template arguments (jit.cpp): the same
 // steps as the interpreted kernel's op loop, with every mask a literal.
 template <int R, int NB, int V, uint32_t XL, uint32_t ZLW, uint32_t CLW, uint32_t SMASK, uint32_t CMASK,
-          uint64_t ZO, uint64_t CO, bool RBI, uint32_t SLOT>
-__device__ __forceinline__ void jit_op(double2 (&v)[1 << R], double2 (&l)[1 << R], uint64_t sbase, uint32_t tbase,
-                                       double ca, double cbb, double kr, double2 ka, double2 kb, const IpSink& sink) {
-  if (CO != 0 && (sbase & CO) != CO) return;
+          uint64_t ZO, uint64_t CO, bool RBI, uint32_t SLOT, bool RET = false>
+__device__ __forceinline__ double jit_op(double2 (&v)[1 << R], double2 (&l)[1 << R], uint64_t sbase, uint32_t tbase,
+                                         double ca, double cbb, double kr, double2 ka, double2 kb, const IpSink& sink) {
+  if (CO != 0 && (sbase & CO) != CO) return 0.0;
   uint32_t slw = 0;
   if (ZLW != 0) slw ^= uint32_t(__popc((tbase ^ XL) & ZLW));
   if (ZO != 0) slw ^= uint32_t(__popcll(sbase & ZO));
@@ -339,7 +343,7 @@ __device__ __forceinline__ void jit_op(double2 (&v)[1 << R], double2 (&l)[1 << R
   c.cmask = CMASK;
   c.clw_ok = (tbase & CLW) == CLW;
   c.pneg = c.bb < 0.0;
-  op_body<R, NB, V>(v, l, c, XL, slw, RBI, SLOT, kr, ka, kb, sink);
+  return op_body<R, NB, V, RET>(v, l, c, XL, slw, RBI, SLOT, kr, ka, kb, sink);
 }
 
 }  // namespace svgb
