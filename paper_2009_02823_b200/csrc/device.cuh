@@ -137,7 +137,7 @@ struct SegDesc {
   uint8_t warppos[8];        // tile positions of warp bits
   double scale;              // SEG_REG: deferred scale C of the register tile at the segment's end
                              // (product of the scaled ops' a since the last flush; kernels_reg.cu upd)
-  double pad_;
+  uint8_t lanepos[8];        // tile positions of lane bits 0..4 (0,1,2,3,4 unless a free-lane plan)
 };
 static_assert(sizeof(SegDesc) == 48, "SegDesc layout");
 

@@ -115,6 +115,21 @@ struct HostBuf {
 
 enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG, L_SWAP, L_FETCH };
 
+// Shared-memory swizzle of a pass's transposes: element e of a tile lives at
+// e ^ sum_{p >= 3, bit p of e set} col[p] (3-bit columns, bits 0..2).  A warp's
+// 16-byte accesses are conflict-free when the columns of the tile positions on
+// lane bits 0..2 are linearly independent (8 distinct 16-byte bank groups per
+// quarter warp).  Positions 0..2 have columns 1, 2, 4 (identity), so the global
+// layout (lanes on positions 0..4) is conflict-free for every choice.
+struct Swizzle {
+  uint8_t col[32] = {1, 2, 4};
+  bool identity() const {
+    for (int p = 3; p < 32; ++p)
+      if (col[p]) return false;
+    return true;
+  }
+};
+
 struct Launch {
   PassDesc d;
   int grid = 0;
@@ -126,6 +141,7 @@ struct Launch {
   bool tiles = false;  // L_REG: stages the tile through shared memory
   int gbit = 0, lpos = 0;  // L_SWAP: rank bit <-> local position
   std::shared_ptr<JitKernel> jit;  // L_REG: circuit-specialised kernel (jit.cu), or null: interpreter
+  Swizzle swz;                     // L_REG: shared-memory swizzle of the pass's transposes
 };
 
 // Everything a sweep needs on the host side, built from one svg_problem.
@@ -134,6 +150,7 @@ struct Lowered {
   int swaps = 0, obs_kernels = 0;
   int64_t swap_bytes = 0;  // bytes each shard exchanges (swaps both ways + partner fetches)
   bool reg = false;  // register-tile kernels in use
+  bool free_lanes_used = false;  // some pass has a segment off the global lane layout (generated kernels only)
   int R = 3;         // their register bits
   std::vector<DevOp> ops;
   std::vector<double2> coef;
@@ -174,6 +191,7 @@ struct svg_engine {
   int64_t opt_pdl = 1;    // generated kernels: programmatic dependent launch
   int64_t opt_fuse_diag = 1;  // generated reverse kernels: fused runs of diagonal rotations
   int64_t opt_acc_prefetch = 1;  // generated reverse kernels: accumulator loads ahead of the op
+  int64_t opt_free_lanes = 1;    // generated kernels: free-lane segment plans where cheaper
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
   // accumulators; 0 = auto (interpreter 24 KB; generated kernels: whatever the
@@ -358,17 +376,75 @@ struct SegLocal {
   }
 };
 
-SegDesc make_seg(int kind, uint32_t regmask, int k, int R, SegLocal* sl) {
+static bool independent3(uint32_t a, uint32_t b, uint32_t c) {
+  return a && b && c && a != b && c != a && c != b && c != (a ^ b);
+}
+
+// Lane order for a lane set: three positions with independent columns first
+// (lane bits 0..2), preferring low positions; false if there are none.
+static bool order_lanes(uint32_t laneset, const Swizzle& sw, uint8_t out[5]) {
+  int pos[5], np = 0;
+  for (uint32_t v = laneset; v && np < 5; v &= v - 1) pos[np++] = __builtin_ctz(v);
+  for (int a = 0; a < np; ++a)
+    for (int b = a + 1; b < np; ++b)
+      for (int c = b + 1; c < np; ++c)
+        if (independent3(sw.col[pos[a]], sw.col[pos[b]], sw.col[pos[c]])) {
+          out[0] = uint8_t(pos[a]);
+          out[1] = uint8_t(pos[b]);
+          out[2] = uint8_t(pos[c]);
+          int o = 3;
+          for (int d = 0; d < np; ++d)
+            if (d != a && d != b && d != c) out[o++] = uint8_t(pos[d]);
+          return true;
+        }
+  for (int d = 0; d < np; ++d) out[d] = uint8_t(pos[d]);
+  return false;
+}
+
+// Swizzle for a pass whose segments use these lane sets (identity when every
+// segment keeps the global lanes).  Deterministic search; on failure the
+// cyclic assignment (some 2-way bank conflicts).
+static Swizzle choose_swizzle(const std::vector<uint32_t>& lanesets, int k) {
+  Swizzle sw;
+  bool all_std = true;
+  for (uint32_t l : lanesets) all_std = all_std && l == 31u;
+  if (all_std) return sw;
+  uint32_t rng = 0x9e3779b9u;
+  for (int t = 0; t < 256; ++t) {
+    Swizzle c;
+    for (int p = 3; p < k; ++p) {
+      if (t == 0) {
+        c.col[p] = uint8_t(((p - 3) % 7) + 1);
+      } else {
+        rng = rng * 1664525u + 1013904223u;
+        c.col[p] = uint8_t(1 + (rng >> 24) % 7);
+      }
+    }
+    bool ok = true;
+    uint8_t tmp[5];
+    for (uint32_t l : lanesets) ok = ok && order_lanes(l, c, tmp);
+    if (ok) return c;
+    if (t == 0) sw = c;
+  }
+  return sw;
+}
+
+SegDesc make_seg(int kind, uint32_t regmask, uint32_t lanemask, const Swizzle& swz, int k, int R, SegLocal* sl) {
   sl->R = R;
   SegDesc sd;
   std::memset(&sd, 0, sizeof(sd));
   sd.scale = 1.0;
   sd.kind = kind;
+  uint8_t lp[5] = {0, 1, 2, 3, 4};
+  if (lanemask != 31u) order_lanes(lanemask, swz, lp);
+  for (int i = 0; i < 5; ++i) {
+    sd.lanepos[i] = lp[i];
+    sl->bit[lp[i]] = static_cast<uint8_t>(i);
+  }
   int r = 0, w = 0;
   for (int pos = 0; pos < k; ++pos) {
-    if (pos < 5) {
-      sl->bit[pos] = static_cast<uint8_t>(pos);
-    } else if ((regmask >> pos) & 1) {
+    if ((lanemask >> pos) & 1) continue;
+    if ((regmask >> pos) & 1) {
       sd.regpos[r] = static_cast<uint8_t>(pos);
       sl->bit[pos] = static_cast<uint8_t>(5 + r++);
     } else {
@@ -518,17 +594,17 @@ bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
 
 std::vector<Segment> memo_segments(const svg_engine* e, const std::vector<uint32_t>& flips,
                                    const std::vector<uint32_t>& touch, const std::vector<char>& dense, int k,
-                                   int regbits) {
+                                   int regbits, bool free = false) {
   std::string key;
-  key.reserve(8 + flips.size() * 9);
-  const int32_t head[] = {k, regbits};
+  key.reserve(12 + flips.size() * 9);
+  const int32_t head[] = {k, regbits, free ? 1 : 0};
   key.append(reinterpret_cast<const char*>(head), sizeof(head));
   key.append(reinterpret_cast<const char*>(flips.data()), flips.size() * 4);
   key.append(reinterpret_cast<const char*>(touch.data()), touch.size() * 4);
   key.append(dense.data(), dense.size());
   auto it = e->seg_memo.find(key);
   if (it != e->seg_memo.end()) return it->second;
-  std::vector<Segment> segs = plan_segments(flips, touch, dense, k, regbits);
+  std::vector<Segment> segs = free ? plan_segments_free(flips, touch, k, regbits) : plan_segments(flips, touch, dense, k, regbits);
   if (e->seg_memo.size() > 16384) e->seg_memo.clear();
   e->seg_memo.emplace(std::move(key), segs);
   return segs;
@@ -657,6 +733,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   SVGB_PHASE(2);
   // segments per pass (register path)
   std::vector<std::vector<Segment>> psegs(steps.size()), psegs_f(steps.size());
+  std::vector<Swizzle> pswz(steps.size()), pswz_f(steps.size());
+  // free-lane plans need the generated kernels (the interpreter keeps lanes on
+  // tile positions 0..4) and tile staging (a first segment off the global layout
+  // reads its tile from the staged copy)
+  const bool free_lanes = L.reg && e->opt_free_lanes && e->opt_stage &&
+                          (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) && jit_available(nullptr);
   if (L.reg) {
     for (size_t si = 0; si < steps.size(); ++si) {
       if (steps[si].swap) continue;
@@ -671,6 +753,26 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
       psegs[si] = memo_segments(e, flips, touch, dense, L.k, RB);
       psegs_f[si] = RF == RB ? psegs[si] : memo_segments(e, flips, touch, dense, L.k, RF);
+      // free-lane plans (generated kernels): every flip in registers, layouts
+      // changed by transposes -- taken per pass and direction when cheaper
+      bool free_ok = free_lanes;
+      for (size_t j = 0; j < ps.items.size() && free_ok; ++j) free_ok = !dense[j] && __builtin_popcount(flips[j]) <= 1;
+      if (free_ok) {
+        // register-op units per amplitude pass: lane flip = 2 (fwd: 1) buffers of shuffles
+        // (4 SHFL per 16-byte amplitude at half the DFMA rate), transpose = 32 B of
+        // shared-memory traffic per amplitude and buffer (measured on the pass model)
+        const std::vector<Segment> fr = memo_segments(e, flips, touch, dense, L.k, RB, true);
+        if (segment_plan_cost(fr, flips, 3.7, 5.3) < segment_plan_cost(psegs[si], flips, 3.7, 5.3)) psegs[si] = fr;
+        const std::vector<Segment> ff = RF == RB ? fr : memo_segments(e, flips, touch, dense, L.k, RF, true);
+        if (segment_plan_cost(ff, flips, 5.0, 8.0) < segment_plan_cost(psegs_f[si], flips, 5.0, 8.0)) psegs_f[si] = ff;
+      }
+      for (const Segment& sg : psegs[si]) L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
+      for (const Segment& sg : psegs_f[si]) L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
+      std::vector<uint32_t> ls, lsf;
+      for (const Segment& sg : psegs[si]) ls.push_back(sg.lanemask);
+      for (const Segment& sg : psegs_f[si]) lsf.push_back(sg.lanemask);
+      pswz[si] = choose_swizzle(ls, L.k);
+      pswz_f[si] = choose_swizzle(lsf, L.k);
     }
   }
   auto reg_launch = [&](const Pass& ps, int nb) {
@@ -715,13 +817,16 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       L.fwd.push_back(l);
     } else {
       Launch l = reg_launch(ps, 1);
-      uint32_t prev = ~0u;
+      l.swz = pswz_f[si];
+      uint32_t prev = ~0u, prev_l = ~0u;
       double C = 1.0;  // deferred scale; flushed when the layout changes (see SegDesc.scale)
       for (const Segment& sg : psegs_f[si]) {
         SegLocal sl;
-        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF), L.k, RF, &sl);
-        sd.same_map = sg.reg && sg.regmask == prev;
+        SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF),
+                              sg.reg ? sg.lanemask : 31u, l.swz, L.k, RF, &sl);
+        sd.same_map = sg.reg && sg.regmask == prev && sg.lanemask == prev_l;
         prev = sg.reg ? sg.regmask : ~0u;
+        prev_l = sg.reg ? sg.lanemask : ~0u;
         if (!sd.same_map) C = 1.0;
         if (sg.reg) {
           sd.op_begin = static_cast<int>(L.rops.size());
@@ -735,6 +840,13 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
           l.tiles = true;
         }
         L.segs.push_back(sd);
+      }
+      if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
+        SegLocal sl;
+        SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, L.k, RF, &sl);
+        sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
+        L.segs.push_back(sd);
+        l.tiles = true;
       }
       l.d.seg_end = static_cast<int>(L.segs.size());
       l.d.op_end = static_cast<int>(L.rops.size());
@@ -855,15 +967,18 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         L.rev.push_back(l);
       } else {
         Launch l = reg_launch(ps, 2);
+        l.swz = pswz[si];
         const std::vector<Segment>& sgs = psegs[si];
-        uint32_t prev = ~0u;
+        uint32_t prev = ~0u, prev_l = ~0u;
         double C = 1.0;
         for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
           const Segment& sg = *st;
           SegLocal sl;
-          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RB), L.k, RB, &sl);
-          sd.same_map = sg.reg && sg.regmask == prev;
+          SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RB),
+                                sg.reg ? sg.lanemask : 31u, l.swz, L.k, RB, &sl);
+          sd.same_map = sg.reg && sg.regmask == prev && sg.lanemask == prev_l;
           prev = sg.reg ? sg.regmask : ~0u;
+          prev_l = sg.reg ? sg.lanemask : ~0u;
           if (!sd.same_map) C = 1.0;
           if (sg.reg) {
             sd.op_begin = static_cast<int>(L.rops.size());
@@ -890,6 +1005,13 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
             l.tiles = true;
           }
           L.segs.push_back(sd);
+        }
+        if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
+          SegLocal sl;
+          SegDesc sd = make_seg(SEG_REG, default_regs(RB), 31u, l.swz, L.k, RB, &sl);
+          sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
+          L.segs.push_back(sd);
+          l.tiles = true;
         }
         l.d.seg_end = static_cast<int>(L.segs.size());
         l.d.op_end = static_cast<int>(L.rops.size());
@@ -1027,6 +1149,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       jp.min_blocks = static_cast<int>(l->nb == 2 ? e->opt_jit_blocks_rev : e->opt_jit_blocks_fwd);
       jp.rest = l->d.rest;
       jp.q = l->d.q;
+      jp.swz = l->swz.col;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -1065,7 +1188,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
     } catch (const std::exception& ex) {
       if (e->jit_dry_run && std::string(ex.what()) != "dry run") throw;
-      if (e->opt_jit == 2 && !e->jit_dry_run) throw;
+      if ((e->opt_jit == 2 || L.free_lanes_used) && !e->jit_dry_run) throw;
       e->jit_error = ex.what();  // auto: keep the interpreted kernels
     }
   }
@@ -1589,6 +1712,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "acc_kb") {
     if (value < 0 || value > 200) return fail(SVG_EINVAL, "acc_kb must be in [0 (auto), 200]");
     e->opt_acc_kb = value;
+  } else if (k == "free_lanes") {
+    e->opt_free_lanes = value != 0;
   } else if (k == "acc_prefetch") {
     e->opt_acc_prefetch = value != 0;
   } else if (k == "fuse_diag") {

@@ -36,6 +36,7 @@ struct JitPass {
   int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
   const uint8_t* q = nullptr;        // tile qubits (PassDesc.q)
+  const uint8_t* swz = nullptr;      // shared-memory swizzle columns per tile position (engine.cu Swizzle)
   const SegDesc* segs = nullptr;     // the pass's segments
   int nsegs = 0;
   const RegOp* rops = nullptr;       // the pass's register ops (rops[0] is op_begin)

@@ -291,6 +291,118 @@ std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const 
   return segs;
 }
 
+std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
+                                        int k, int regbits) {
+  const int m = static_cast<int>(flip_pos.size());
+  const uint32_t all = (k >= 32) ? ~0u : ((1u << k) - 1);
+  std::vector<std::vector<int>> succ(m);
+  std::vector<int> npred(m, 0);
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) {
+      const uint32_t shared = touch_pos[i] & touch_pos[j];
+      if (shared & (flip_pos[i] | flip_pos[j])) {
+        succ[i].push_back(j);
+        ++npred[j];
+      }
+    }
+  std::vector<char> done(m, 0);
+  int remaining = m;
+  // gates runnable (transitively) whose flips lie in `regs`
+  auto closure = [&](uint32_t regs, std::vector<int>* order) {
+    std::vector<int> pred = npred;
+    std::vector<char> taken(done);
+    int count = 0;
+    for (bool progress = true; progress;) {
+      progress = false;
+      for (int i = 0; i < m; ++i) {
+        if (taken[i] || pred[i] != 0 || (flip_pos[i] & ~regs)) continue;
+        taken[i] = 1;
+        ++count;
+        progress = true;
+        if (order) order->push_back(i);
+        for (int j : succ[i]) --pred[j];
+      }
+    }
+    return count;
+  };
+  std::vector<Segment> segs;
+  while (remaining > 0) {
+    uint32_t regs = 0;
+    int best_count = closure(0, nullptr);
+    while (popc(regs) < regbits) {
+      uint32_t cand = 0;
+      for (int i = 0; i < m; ++i)
+        if (!done[i]) cand |= flip_pos[i] & all & ~regs;
+      if (!cand) break;
+      int best = -1, best_pos = -1;
+      for (uint32_t v = cand; v; v &= v - 1) {
+        const int p = __builtin_ctz(v);
+        const int c = closure(regs | (1u << p), nullptr);
+        if (c > best || (c == best && p >= 5 && best_pos < 5)) {  // ties: keep 0..4 free for the lanes
+          best = c;
+          best_pos = p;
+        }
+      }
+      if (best <= best_count && popc(regs) > 0) {
+        // no single position unlocks a gate: take the flip set of the earliest ready gate
+        std::vector<int> pred_ready;
+        for (int i = 0; i < m; ++i)
+          if (!done[i] && npred[i] == 0 && popc(regs | flip_pos[i]) <= regbits && (flip_pos[i] & ~regs)) {
+            regs |= flip_pos[i];
+            break;
+          }
+        break;
+      }
+      regs |= 1u << best_pos;
+      best_count = best;
+    }
+    Segment sg;
+    sg.regmask = regs;
+    closure(regs, &sg.items);
+    if (sg.items.empty()) throw std::runtime_error("free-lane segment planner made no progress");
+    for (int i : sg.items) {
+      done[i] = 1;
+      --remaining;
+      for (int j : succ[i]) --npred[j];
+    }
+    segs.push_back(sg);
+  }
+  // Fill register sets to `regbits` (positions the next segments flip first:
+  // fewer distinct layouts), then lanes: 0..4 where free, else the lowest free
+  // positions.  Equal consecutive layouts need no transpose.
+  for (size_t s = 0; s < segs.size(); ++s) {
+    uint32_t& rm = segs[s].regmask;
+    for (size_t t = s + 1; t < segs.size() && popc(rm) < regbits; ++t)
+      for (uint32_t v = segs[t].regmask & ~rm; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+    for (uint32_t v = all & ~rm & ~31u; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+    for (uint32_t v = all & ~rm; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+    uint32_t lanes = 31u & ~rm;
+    for (uint32_t v = all & ~rm & ~lanes; v && popc(lanes) < 5; v &= v - 1) lanes |= v & (~v + 1);
+    segs[s].lanemask = lanes;
+  }
+  return segs;
+}
+
+double segment_plan_cost(const std::vector<Segment>& segs, const std::vector<uint32_t>& flip_pos, double lane_cost,
+                         double xpose_cost) {
+  double c = 0.0;
+  uint32_t prev_r = ~0u, prev_l = ~0u;
+  for (size_t s = 0; s < segs.size(); ++s) {
+    const Segment& sg = segs[s];
+    if (!sg.reg) return 1e30;
+    if (s > 0 && (sg.regmask != prev_r || sg.lanemask != prev_l)) c += xpose_cost;
+    prev_r = sg.regmask;
+    prev_l = sg.lanemask;
+    for (int i : sg.items) {
+      const uint32_t f = flip_pos[i];
+      c += f == 0 ? 0.5 : ((f & sg.lanemask) ? lane_cost : 1.0);
+    }
+  }
+  if (!segs.empty() && segs.back().lanemask != 31u) c += xpose_cost;   // forward store
+  if (!segs.empty() && segs.front().lanemask != 31u) c += xpose_cost;  // reverse store
+  return c;
+}
+
 int choose_tile_qubits(int n, int requested, int sms) {
   if (requested > 0) return std::min(requested, n);
   if (n <= 10) return n;  // whole state in one tile: one CTA, no HBM round trips between passes

@@ -68,11 +68,28 @@ struct Segment {
   bool reg = true;
   std::vector<int> items;   // indices into the pass's item list
   uint32_t regmask = 0;     // tile positions held in registers (reg segments)
+  uint32_t lanemask = 31;   // tile positions on the 32 lanes (free-lane plans; else 0..4)
 };
 // Gates may be reordered inside a pass (dependency-aware list scheduling):
 // each segment takes the register set that unlocks the most pending gates.
 std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
                                    const std::vector<char>& dense, int k, int regbits);
+
+// Free-lane register segments (circuit-specialised kernels only, no dense
+// gates): any `regbits` tile positions may be register bits, and a segment's
+// gates flip register positions only -- no lane flips (a lane flip is a warp
+// shuffle of both buffers, ~3.7x a register op).  Lanes are 5 positions the
+// segment does not flip, preferring tile positions 0..4 (the global layout).
+// Layout changes go through shared memory (transposes).
+std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
+                                        int k, int regbits);
+
+// Relative cost of a segment plan in register-op units (nb buffers): register
+// flips 1, lane flips `lane_cost`, diagonal ops 0.5, each layout change
+// `xpose_cost`; `std_end` adds a final transpose when the last segment's
+// lanes are not tile positions 0..4 (the store needs the global layout).
+double segment_plan_cost(const std::vector<Segment>& segs, const std::vector<uint32_t>& flip_pos, double lane_cost,
+                         double xpose_cost);
 
 // ---- sharded schedules (state split over 2^g ranks by its top g PHYSICAL qubits) ----
 //
