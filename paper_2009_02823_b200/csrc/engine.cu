@@ -151,6 +151,8 @@ struct Lowered {
   int64_t swap_bytes = 0;  // bytes each shard exchanges (swaps both ways + partner fetches)
   bool reg = false;  // register-tile kernels in use
   bool free_lanes_used = false;  // some pass has a segment off the global lane layout (generated kernels only)
+  bool jit_planned = false;      // register passes planned for the generated kernels (deferred scale carried
+                                 // across layout changes, see JitPass.scale_carry)
   int R = 3;         // their register bits
   std::vector<DevOp> ops;
   std::vector<double2> coef;
@@ -192,6 +194,8 @@ struct svg_engine {
   int64_t opt_fuse_diag = 1;  // generated reverse kernels: fused runs of diagonal rotations
   int64_t opt_acc_prefetch = 1;  // generated reverse kernels: accumulator loads ahead of the op
   int64_t opt_free_lanes = 1;    // generated kernels: free-lane segment plans where cheaper
+  int64_t opt_scale_carry = 1;   // generated kernels: deferred scale carried across layout changes
+  int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
   // accumulators; 0 = auto (interpreter 24 KB; generated kernels: whatever the
@@ -737,8 +741,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // free-lane plans need the generated kernels (the interpreter keeps lanes on
   // tile positions 0..4) and tile staging (a first segment off the global layout
   // reads its tile from the staged copy)
-  const bool free_lanes = L.reg && e->opt_free_lanes && e->opt_stage &&
-                          (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) && jit_available(nullptr);
+  const bool jit_planned = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) &&
+                           (e->jit_dry_run || jit_available(nullptr));
+  const bool free_lanes = jit_planned && e->opt_free_lanes && e->opt_stage;
+  L.jit_planned = jit_planned;
   if (L.reg) {
     for (size_t si = 0; si < steps.size(); ++si) {
       if (steps[si].swap) continue;
@@ -761,8 +767,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         // register-op units per amplitude pass: lane flip = 2 (fwd: 1) buffers of shuffles
         // (4 SHFL per 16-byte amplitude at half the DFMA rate), transpose = 32 B of
         // shared-memory traffic per amplitude and buffer (measured on the pass model)
+        const double lc = 0.1 * double(e->opt_lane_cost10), xc = 0.1 * double(e->opt_xpose_cost10);
         const std::vector<Segment> fr = memo_segments(e, flips, touch, dense, L.k, RB, true);
-        if (segment_plan_cost(fr, flips, 3.7, 5.3) < segment_plan_cost(psegs[si], flips, 3.7, 5.3)) psegs[si] = fr;
+        if (segment_plan_cost(fr, flips, lc, xc) < segment_plan_cost(psegs[si], flips, lc, xc)) psegs[si] = fr;
         const std::vector<Segment> ff = RF == RB ? fr : memo_segments(e, flips, touch, dense, L.k, RF, true);
         if (segment_plan_cost(ff, flips, 5.0, 8.0) < segment_plan_cost(psegs_f[si], flips, 5.0, 8.0)) psegs_f[si] = ff;
       }
@@ -796,6 +803,15 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // default register layout for shared-memory segments: lowest non-lane positions
   auto default_regs = [](int R) { return ((1u << (5 + R)) - 1u) & ~31u; };
 
+  // generated kernels keep the deferred scale C across layout changes (one
+  // flush per tile, at the store) when a pass has no shared-memory segments
+  const bool carry = jit_planned && e->opt_scale_carry;
+  auto all_reg = [](const std::vector<Segment>& v) {
+    for (const Segment& sg : v)
+      if (!sg.reg) return false;
+    return true;
+  };
+
   SVGB_PHASE(3);
   // forward schedule
   for (size_t si = 0; si < steps.size(); ++si) {
@@ -827,7 +843,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         sd.same_map = sg.reg && sg.regmask == prev && sg.lanemask == prev_l;
         prev = sg.reg ? sg.regmask : ~0u;
         prev_l = sg.reg ? sg.lanemask : ~0u;
-        if (!sd.same_map) C = 1.0;
+        if (!sd.same_map && !(carry && all_reg(psegs_f[si]))) C = 1.0;
         if (sg.reg) {
           sd.op_begin = static_cast<int>(L.rops.size());
           for (int it : sg.items) emit_rop(L, tm, sl, gs[it], ROP_FWD, gs[it].fwd, nullptr, 0, real_sums, &C);
@@ -845,6 +861,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         SegLocal sl;
         SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, L.k, RF, &sl);
         sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
+        sd.scale = carry ? C : 1.0;
         L.segs.push_back(sd);
         l.tiles = true;
       }
@@ -979,7 +996,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
           sd.same_map = sg.reg && sg.regmask == prev && sg.lanemask == prev_l;
           prev = sg.reg ? sg.regmask : ~0u;
           prev_l = sg.reg ? sg.lanemask : ~0u;
-          if (!sd.same_map) C = 1.0;
+          if (!sd.same_map && !(carry && all_reg(sgs))) C = 1.0;
           if (sg.reg) {
             sd.op_begin = static_cast<int>(L.rops.size());
             for (auto it = sg.items.rbegin(); it != sg.items.rend(); ++it) {
@@ -1010,6 +1027,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
           SegLocal sl;
           SegDesc sd = make_seg(SEG_REG, default_regs(RB), 31u, l.swz, L.k, RB, &sl);
           sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
+          sd.scale = carry ? C : 1.0;
           L.segs.push_back(sd);
           l.tiles = true;
         }
@@ -1150,6 +1168,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       jp.rest = l->d.rest;
       jp.q = l->d.q;
       jp.swz = l->swz.col;
+      jp.scale_carry = carry;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -1188,7 +1207,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
     } catch (const std::exception& ex) {
       if (e->jit_dry_run && std::string(ex.what()) != "dry run") throw;
-      if ((e->opt_jit == 2 || L.free_lanes_used) && !e->jit_dry_run) throw;
+      if ((e->opt_jit == 2 || L.free_lanes_used || carry) && !e->jit_dry_run) throw;
       e->jit_error = ex.what();  // auto: keep the interpreted kernels
     }
   }
@@ -1712,6 +1731,11 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "acc_kb") {
     if (value < 0 || value > 200) return fail(SVG_EINVAL, "acc_kb must be in [0 (auto), 200]");
     e->opt_acc_kb = value;
+  } else if (k == "lane_cost10" || k == "xpose_cost10") {
+    if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
+    (k == "lane_cost10" ? e->opt_lane_cost10 : e->opt_xpose_cost10) = value;
+  } else if (k == "scale_carry") {
+    e->opt_scale_carry = value != 0;
   } else if (k == "free_lanes") {
     e->opt_free_lanes = value != 0;
   } else if (k == "acc_prefetch") {

@@ -32,6 +32,7 @@ struct JitPass {
   int acc_shift = 0;                 // thread_acc: lanes combined per accumulator (log2)
   bool fuse_diag = true;             // reverse passes: fuse runs of diagonal rotations
   bool acc_prefetch = true;          // reverse passes: load an op's accumulator before the op
+  bool scale_carry = false;          // deferred scale carried across layout changes (no shared-memory segments)
   bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
   int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
