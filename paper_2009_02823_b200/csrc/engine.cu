@@ -195,6 +195,7 @@ struct svg_engine {
   int64_t opt_acc_prefetch = 1;  // generated reverse kernels: accumulator loads ahead of the op
   int64_t opt_free_lanes = 1;    // generated kernels: free-lane segment plans where cheaper
   int64_t opt_scale_carry = 1;   // generated kernels: deferred scale carried across layout changes
+  int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
   int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
@@ -470,6 +471,8 @@ constexpr int kJitMinQubits = 18;
 // Gates per register-tile pass: beyond ~40 the straight-line pass kernels
 // outgrow the instruction cache (measured: cfg 3 reverse 115 ms at 96, 105 ms at 40).
 constexpr int kRegPassGates = 40;
+// Forward sweeps of states this large run their own schedule over k+1-qubit tiles.
+constexpr int kFwdSplitQubits = 24;
 
 // One register op for gate g: operator coefficients `c` (a, b of a I + b P),
 // optionally fused with the post-gate generator `kpost` into `slot`.
@@ -688,11 +691,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   std::vector<GateShape> logical(p->num_gates);
   for (int i = 0; i < p->num_gates; ++i) logical[i] = gate_shape(p->gates[i]);
   std::vector<int> l2p_final;
-  std::vector<Step> steps;
-  {  // the schedule is a pure function of the gate shapes and plan parameters: memoised
+  // the schedule is a pure function of the gate shapes and plan parameters: memoised
+  auto schedule = [&](const PlanParams& pq, std::vector<int>* l2p_out) {
     std::string key;
     key.reserve(32 + logical.size() * sizeof(GateShape));
-    const int32_t head[] = {n, g, pp.n, pp.k, pp.b, pp.max_items, pp.max_derivs};
+    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs};
     key.append(reinterpret_cast<const char*>(head), sizeof(head));
     for (const GateShape& sh : logical) {
       key.append(reinterpret_cast<const char*>(&sh.flip), 8);
@@ -701,14 +704,41 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     }
     auto it = e->plan_memo.find(key);
     if (it != e->plan_memo.end()) {
-      steps = it->second.first;
-      l2p_final = it->second.second;
+      if (l2p_out) *l2p_out = it->second.second;
+      return it->second.first;
+    }
+    std::vector<int> l2p;
+    std::vector<Step> st = plan_schedule(logical, n, g, pq, &l2p);
+    if (e->plan_memo.size() > 64) e->plan_memo.clear();
+    e->plan_memo.emplace(std::move(key), std::make_pair(st, l2p));
+    if (l2p_out) *l2p_out = l2p;
+    return st;
+  };
+  const std::vector<Step> steps = schedule(pp, &l2p_final);
+  // free-lane plans and carried scales need the generated kernels (the
+  // interpreter keeps lanes on tile positions 0..4)
+  const bool jit_planned = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) &&
+                           (e->jit_dry_run || jit_available(nullptr));
+  L.jit_planned = jit_planned;
+  // The forward sweep only has to deliver psi at its end, so (one shard, generated
+  // kernels) it runs its own schedule over larger tiles -- one buffer per tile
+  // leaves room for 2^(k+1) amplitudes per CTA: fewer HBM passes.
+  int kf = L.k;
+  std::vector<Step> steps_fsplit;
+  // (auto: states of >= kFwdSplitQubits qubits, whose passes stream HBM; smaller,
+  // L2-resident states are better served by more, smaller tiles -- measured cfg 2)
+  if (g == 0 && jit_planned && nloc > L.k && (e->opt_tile_fwd > 0 || (e->opt_tile_fwd == 0 && nloc >= kFwdSplitQubits))) {
+    kf = e->opt_tile_fwd > 0 ? static_cast<int>(e->opt_tile_fwd) : L.k + 1;
+    kf = std::max(L.k, std::min({kf, nloc, 13}));
+    if (kf > L.k) {
+      PlanParams pq = pp;
+      pq.k = kf;
+      steps_fsplit = schedule(pq, nullptr);
     } else {
-      steps = plan_schedule(logical, n, g, pp, &l2p_final);
-      if (e->plan_memo.size() > 64) e->plan_memo.clear();
-      e->plan_memo.emplace(std::move(key), std::make_pair(steps, l2p_final));
+      kf = L.k;
     }
   }
+  const std::vector<Step>& fsteps = kf > L.k ? steps_fsplit : steps;
   // physical gates per pass step, parallel to the step's items
   std::vector<GateList> pgates(steps.size());
   std::deque<svg_gate> pstore;  // remapped copies (only when the qubit map is not the identity)
@@ -728,6 +758,20 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     }
   }
 
+  std::vector<GateList> pgates_fs;
+  std::vector<std::vector<GateShape>> pshapes_fs;
+  if (&fsteps != &steps) {  // one shard: identity qubit map
+    pgates_fs.resize(fsteps.size());
+    pshapes_fs.resize(fsteps.size());
+    for (size_t si = 0; si < fsteps.size(); ++si)
+      for (int gi : fsteps[si].pass.items) {
+        pgates_fs[si].ptr.push_back(&p->gates[gi]);
+        pshapes_fs[si].push_back(logical[gi]);
+      }
+  }
+  const std::vector<GateList>& fpgates = &fsteps != &steps ? pgates_fs : pgates;
+  const std::vector<std::vector<GateShape>>& fpshapes = &fsteps != &steps ? pshapes_fs : pshapes;
+
   std::vector<int> first_deriv(p->num_gates + 1, 0);
   for (int i = 0; i < p->num_gates; ++i) first_deriv[i + 1] = first_deriv[i] + p->gates[i].nderiv;
   SVGB_PHASE(1);
@@ -736,59 +780,56 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   SVGB_PHASE(2);
   // segments per pass (register path)
-  std::vector<std::vector<Segment>> psegs(steps.size()), psegs_f(steps.size());
-  std::vector<Swizzle> pswz(steps.size()), pswz_f(steps.size());
-  // free-lane plans need the generated kernels (the interpreter keeps lanes on
-  // tile positions 0..4) and tile staging (a first segment off the global layout
-  // reads its tile from the staged copy)
-  const bool jit_planned = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) &&
-                           (e->jit_dry_run || jit_available(nullptr));
+  std::vector<std::vector<Segment>> psegs(steps.size()), psegs_f(fsteps.size());
+  std::vector<Swizzle> pswz(steps.size()), pswz_f(fsteps.size());
+  // free-lane plans also need tile staging (a first segment off the global
+  // layout reads its tile from the staged copy)
   const bool free_lanes = jit_planned && e->opt_free_lanes && e->opt_stage;
-  L.jit_planned = jit_planned;
-  if (L.reg) {
-    for (size_t si = 0; si < steps.size(); ++si) {
-      if (steps[si].swap) continue;
-      const Pass& ps = steps[si].pass;
-      const TileMap tm = tile_map(ps.qmask);
-      std::vector<uint32_t> flips(ps.items.size()), touch(ps.items.size());
-      std::vector<char> dense(ps.items.size());
-      for (size_t j = 0; j < ps.items.size(); ++j) {
-        flips[j] = tm.local(pshapes[si][j].flip);
-        touch[j] = tm.local(pshapes[si][j].touch);
-        dense[j] = !reg_capable(pgates[si][j], flips[j]);
-      }
-      psegs[si] = memo_segments(e, flips, touch, dense, L.k, RB);
-      psegs_f[si] = RF == RB ? psegs[si] : memo_segments(e, flips, touch, dense, L.k, RF);
-      // free-lane plans (generated kernels): every flip in registers, layouts
-      // changed by transposes -- taken per pass and direction when cheaper
-      bool free_ok = free_lanes;
-      for (size_t j = 0; j < ps.items.size() && free_ok; ++j) free_ok = !dense[j] && __builtin_popcount(flips[j]) <= 1;
-      if (free_ok) {
-        // register-op units per amplitude pass: lane flip = 2 (fwd: 1) buffers of shuffles
-        // (4 SHFL per 16-byte amplitude at half the DFMA rate), transpose = 32 B of
-        // shared-memory traffic per amplitude and buffer (measured on the pass model)
-        const double lc = 0.1 * double(e->opt_lane_cost10), xc = 0.1 * double(e->opt_xpose_cost10);
-        const std::vector<Segment> fr = memo_segments(e, flips, touch, dense, L.k, RB, true);
-        if (segment_plan_cost(fr, flips, lc, xc) < segment_plan_cost(psegs[si], flips, lc, xc)) psegs[si] = fr;
-        const std::vector<Segment> ff = RF == RB ? fr : memo_segments(e, flips, touch, dense, L.k, RF, true);
-        if (segment_plan_cost(ff, flips, 5.0, 8.0) < segment_plan_cost(psegs_f[si], flips, 5.0, 8.0)) psegs_f[si] = ff;
-      }
-      for (const Segment& sg : psegs[si]) L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
-      for (const Segment& sg : psegs_f[si]) L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
-      std::vector<uint32_t> ls, lsf;
-      for (const Segment& sg : psegs[si]) ls.push_back(sg.lanemask);
-      for (const Segment& sg : psegs_f[si]) lsf.push_back(sg.lanemask);
-      pswz[si] = choose_swizzle(ls, L.k);
-      pswz_f[si] = choose_swizzle(lsf, L.k);
+  // segments of one pass at tile width kk with R register bits: the fixed-lane
+  // plan, or the free-lane plan when the cost model prefers it (lc: lane op,
+  // xc: layout change, in register-op units)
+  auto pass_segments = [&](const Pass& ps, const GateList& gl, const std::vector<GateShape>& shp, int kk, int R,
+                           double lc, double xc, std::vector<Segment>* out, Swizzle* swz) {
+    const TileMap tm = tile_map(ps.qmask);
+    std::vector<uint32_t> flips(ps.items.size()), touch(ps.items.size());
+    std::vector<char> dense(ps.items.size());
+    for (size_t j = 0; j < ps.items.size(); ++j) {
+      flips[j] = tm.local(shp[j].flip);
+      touch[j] = tm.local(shp[j].touch);
+      dense[j] = !reg_capable(gl[j], flips[j]);
     }
+    *out = memo_segments(e, flips, touch, dense, kk, R);
+    bool free_ok = free_lanes;
+    for (size_t j = 0; j < ps.items.size() && free_ok; ++j) free_ok = !dense[j] && __builtin_popcount(flips[j]) <= 1;
+    if (free_ok) {
+      std::vector<Segment> fr = memo_segments(e, flips, touch, dense, kk, R, true);
+      if (segment_plan_cost(fr, flips, lc, xc) < segment_plan_cost(*out, flips, lc, xc)) *out = std::move(fr);
+    }
+    std::vector<uint32_t> ls;
+    for (const Segment& sg : *out) {
+      ls.push_back(sg.lanemask);
+      L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
+    }
+    *swz = choose_swizzle(ls, kk);
+  };
+  if (L.reg) {
+    // register-op units per amplitude: a lane flip is a warp shuffle of both (fwd:
+    // one) buffers (4 SHFL per 16-byte amplitude at half the DFMA rate), a layout
+    // change 32 B of shared-memory traffic per amplitude and buffer
+    const double lc = 0.1 * double(e->opt_lane_cost10), xc = 0.1 * double(e->opt_xpose_cost10);
+    for (size_t si = 0; si < steps.size(); ++si)
+      if (!steps[si].swap) pass_segments(steps[si].pass, pgates[si], pshapes[si], L.k, RB, lc, xc, &psegs[si], &pswz[si]);
+    for (size_t si = 0; si < fsteps.size(); ++si)
+      if (!fsteps[si].swap)
+        pass_segments(fsteps[si].pass, fpgates[si], fpshapes[si], kf, RF, 5.0, 8.0, &psegs_f[si], &pswz_f[si]);
   }
-  auto reg_launch = [&](const Pass& ps, int nb) {
+  auto reg_launch = [&](const Pass& ps, int nb, int kk) {
     Launch l;
-    l.d = make_desc(nloc, L.k, ps.qmask);
+    l.d = make_desc(nloc, kk, ps.qmask);
     l.kind = L_REG;
     l.nb = nb;
     l.R = nb == 1 ? RF : RB;
-    l.threads = 32 << (L.k - 5 - l.R);
+    l.threads = 32 << (kk - 5 - l.R);
     l.d.seg_begin = static_cast<int>(L.segs.size());
     l.d.op_begin = static_cast<int>(L.rops.size());  // this pass's register ops (staged in smem)
     return l;
@@ -814,14 +855,14 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   SVGB_PHASE(3);
   // forward schedule
-  for (size_t si = 0; si < steps.size(); ++si) {
-    if (steps[si].swap) {
-      L.fwd.push_back(swap_launch(steps[si]));
+  for (size_t si = 0; si < fsteps.size(); ++si) {
+    if (fsteps[si].swap) {
+      L.fwd.push_back(swap_launch(fsteps[si]));
       L.swap_bytes += S;  // half a shard out, half in
       continue;
     }
-    const Pass& ps = steps[si].pass;
-    const GateList& gs = pgates[si];
+    const Pass& ps = fsteps[si].pass;
+    const GateList& gs = fpgates[si];
     const TileMap tm = tile_map(ps.qmask);
     if (!L.reg) {
       Launch l;
@@ -832,14 +873,14 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       l.d.op_end = static_cast<int>(L.ops.size());
       L.fwd.push_back(l);
     } else {
-      Launch l = reg_launch(ps, 1);
+      Launch l = reg_launch(ps, 1, kf);
       l.swz = pswz_f[si];
       uint32_t prev = ~0u, prev_l = ~0u;
       double C = 1.0;  // deferred scale; flushed when the layout changes (see SegDesc.scale)
       for (const Segment& sg : psegs_f[si]) {
         SegLocal sl;
         SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF),
-                              sg.reg ? sg.lanemask : 31u, l.swz, L.k, RF, &sl);
+                              sg.reg ? sg.lanemask : 31u, l.swz, kf, RF, &sl);
         sd.same_map = sg.reg && sg.regmask == prev && sg.lanemask == prev_l;
         prev = sg.reg ? sg.regmask : ~0u;
         prev_l = sg.reg ? sg.lanemask : ~0u;
@@ -859,7 +900,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
       if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
         SegLocal sl;
-        SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, L.k, RF, &sl);
+        SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, kf, RF, &sl);
         sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
         sd.scale = carry ? C : 1.0;
         L.segs.push_back(sd);
@@ -983,7 +1024,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         l.d.nslots = static_cast<int>(slot);
         L.rev.push_back(l);
       } else {
-        Launch l = reg_launch(ps, 2);
+        Launch l = reg_launch(ps, 2, L.k);
         l.swz = pswz[si];
         const std::vector<Segment>& sgs = psegs[si];
         uint32_t prev = ~0u, prev_l = ~0u;
@@ -1043,7 +1084,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   SVGB_PHASE(6);
   // grids, shared memory, partial offsets
-  const int64_t ntiles = int64_t(1) << (nloc - L.k);
+  auto ntiles_of = [&](const Launch& l) { return int64_t(1) << (nloc - (l.kind == L_REG ? l.d.k : L.k)); };
   // lane-group inner-product accumulators: combine 2^shift lanes so that the
   // shared accumulators stay within 24 KB (two 128-thread CTAs with 64 KB of
   // transpose tiles still fit an SM; no per-op full warp reductions)
@@ -1062,10 +1103,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     e->occ_memo[key] = v;
     return v;
   };
-  auto clamp_grid = [&](int per_sm) {
+  auto clamp_grid_k = [&](int per_sm, int64_t ntiles) {
     const int64_t slots = int64_t(e->sms) * per_sm;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, slots)));
   };
+  const int64_t ntiles_std = int64_t(1) << (nloc - L.k);
+  auto clamp_grid = [&](int per_sm) { return clamp_grid_k(per_sm, ntiles_std); };
   auto size_launch = [&](Launch& l) {
     switch (l.kind) {
       case L_SMEM_FWD:
@@ -1090,7 +1133,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
             }
             l.jit->blocks_per_sm = blocks;
           }
-          l.grid = clamp_grid(l.jit->blocks_per_sm);
+          l.grid = clamp_grid_k(l.jit->blocks_per_sm, ntiles_of(l));
           break;
         }
         l.smem = reg_smem(L.k, l.nb, l.threads / 32, l.d.nslots, l.d.op_end - l.d.op_begin,
@@ -1145,7 +1188,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         const int blocks = l->nb == 2 ? (e->opt_jit_blocks_rev ? int(e->opt_jit_blocks_rev) : 2)
                                       : (e->opt_jit_blocks_fwd ? int(e->opt_jit_blocks_fwd) : (l->R == 3 ? 2 : 4));
         const size_t share = std::min<size_t>(e->max_smem, (size_t(e->max_smem_sm) / blocks) - 1024);
-        const size_t fixed = (sizeof(double2) << L.k) * l->nb + sizeof(double2) * (l->threads / 32) * l->d.nslots;
+        const size_t fixed = (sizeof(double2) << l->d.k) * l->nb + sizeof(double2) * (l->threads / 32) * l->d.nslots;
         const size_t budget = share > fixed + 4096 ? share - fixed : 4096;
         l->d.acc_shift = 0;
         while (l->d.acc_shift < 5 && size_t(l->d.nslots) * (l->threads >> l->d.acc_shift) * sizeof(double) > budget)
@@ -1154,7 +1197,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       JitPass jp;
       jp.R = l->R;
       jp.nb = l->nb;
-      jp.k = L.k;
+      jp.k = l->d.k;
       jp.nloc = nloc;
       jp.threads = l->threads;
       jp.nslots = l->d.nslots;
@@ -1734,6 +1777,9 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "lane_cost10" || k == "xpose_cost10") {
     if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
     (k == "lane_cost10" ? e->opt_lane_cost10 : e->opt_xpose_cost10) = value;
+  } else if (k == "tile_fwd") {
+    if (value < -1 || value > 13) return fail(SVG_EINVAL, "tile_fwd must be in [-1, 13]");
+    e->opt_tile_fwd = value;
   } else if (k == "scale_carry") {
     e->opt_scale_carry = value != 0;
   } else if (k == "free_lanes") {
@@ -1829,6 +1875,15 @@ extern "C" int svg_debug_jit_check(const svg_problem* p, const int64_t* opts, in
   } catch (const std::exception& ex) {
     return fail(SVG_EINVAL, ex.what());
   }
+}
+
+// Debug / profiling (not in the public header): per-phase host milliseconds of
+// lower() accumulated on the calling thread since the last reset (out_ms[0..8]).
+extern "C" int svg_debug_phase_ms(double* out_ms, int reset) {
+  for (int i = 0; i < 9; ++i) out_ms[i] = g_phase_ms[i];
+  if (reset)
+    for (double& v : g_phase_ms) v = 0.0;
+  return SVG_OK;
 }
 
 // Debug / profiling (not in the public header): host-only lowering of `p`
