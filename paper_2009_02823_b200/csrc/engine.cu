@@ -665,13 +665,17 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   const bool real_sums = (p->flags & SVG_FLAG_REAL_SUMS) != 0;
   L.n = n;
   L.nloc = nloc;
-  L.k = choose_tile_qubits(nloc, static_cast<int>(e->opt_tile), e->sms);
+  // generated kernels (shards of >= kJitMinQubits): two tiles per SM suffice
+  // (one CTA pair); wider tiles mean fewer passes (measured cfg 2: k 11 / R 4 6 % faster)
+  const bool jit_expected = e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits);
+  L.k = choose_tile_qubits(nloc, static_cast<int>(e->opt_tile), e->sms, jit_expected ? 2 : 4);
   L.b = (nloc <= L.k) ? nloc : std::min(5, L.k - 2);
   if (g > 0 && L.b < 5 && nloc > L.k) throw InvalidArg("sharded engines need >= 7 qubits per shard");
-  // register bits (amplitudes per thread per buffer = 2^R): auto = 3 for shards of
-  // <= 23 qubits (more threads per tile: better latency hiding when a pass is only
-  // a few tile rounds), 4 above (fewer ops per amplitude; measured cfg 2 / cfg 3)
-  const int Rauto = nloc <= 23 ? 3 : 4;
+  // register bits (amplitudes per thread per buffer = 2^R): auto = 4 for the
+  // generated kernels (fewer ops per amplitude; measured cfg 2 / cfg 3); the
+  // interpreter keeps 3 for shards of <= 23 qubits (more threads per tile: better
+  // latency hiding when a pass is only a few tile rounds)
+  const int Rauto = (nloc <= 23 && !jit_expected) ? 3 : 4;
   const int RB = e->opt_reg_bits ? static_cast<int>(e->opt_reg_bits) : Rauto;          // reverse passes
   const int RF = e->opt_reg_bits_fwd ? static_cast<int>(e->opt_reg_bits_fwd) : Rauto;  // forward passes
   L.R = RB;

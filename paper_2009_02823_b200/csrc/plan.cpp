@@ -403,12 +403,12 @@ double segment_plan_cost(const std::vector<Segment>& segs, const std::vector<uin
   return c;
 }
 
-int choose_tile_qubits(int n, int requested, int sms) {
+int choose_tile_qubits(int n, int requested, int sms, int min_tiles_per_sm) {
   if (requested > 0) return std::min(requested, n);
   if (n <= 10) return n;  // whole state in one tile: one CTA, no HBM round trips between passes
   int k = std::min(n, 11);
-  // keep at least ~4 tiles per SM so the persistent grid stays balanced
-  while (k > 9 && (n - k) < 62 && (1ll << (n - k)) < 4ll * sms) --k;
+  // keep at least a few tiles per SM so the persistent grid stays balanced
+  while (k > 9 && (n - k) < 62 && (1ll << (n - k)) < int64_t(min_tiles_per_sm) * sms) --k;
   return std::min(k, n);
 }
 

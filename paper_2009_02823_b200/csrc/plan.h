@@ -113,7 +113,8 @@ uint64_t remap_mask(uint64_t m, const std::vector<int>& l2p);
 std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, int g, const PlanParams& pp,
                                 std::vector<int>* l2p_final);
 
-// Tile size choice for n qubits on `sms` SMs (auto when requested == 0).
-int choose_tile_qubits(int n, int requested, int sms);
+// Tile size choice for n qubits on `sms` SMs (auto when requested == 0): the
+// widest tile (<= 11 qubits) leaving >= min_tiles_per_sm tiles per SM.
+int choose_tile_qubits(int n, int requested, int sms, int min_tiles_per_sm = 4);
 
 }  // namespace svgb
