@@ -1332,6 +1332,18 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     const auto t_enter = std::chrono::steady_clock::now();
     validate(p);
     CK(cudaSetDevice(e->device));
+    // A host input state starts its (large) host -> device copy before the host-side
+    // lowering, which then overlaps the transfer; shards are consecutive slices of
+    // the full index range (identity layout at the start).
+    bool input_copied = false;
+    if (p->input_amps) {
+      const size_t amps0 = (size_t(1) << (p->num_qubits - e->shard_bits)) * e->shards_local;
+      const size_t first0 = e->comm ? size_t(e->rank) * (size_t(1) << (p->num_qubits - e->shard_bits)) : 0;
+      e->psi.reserve(amps0 * sizeof(double2));
+      CK(cudaMemcpyAsync(e->psi.ptr, p->input_amps + first0, amps0 * sizeof(double2), cudaMemcpyHostToDevice,
+                         e->stream));
+      input_copied = true;
+    }
     const Lowered L = lower(e, p, with_reverse);
     const auto t_lowered = std::chrono::steady_clock::now();
     const int nloc = L.nloc;
@@ -1461,7 +1473,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     // input: shards are consecutive slices of the full index range (identity layout at the start)
     const size_t first_amp = e->comm ? size_t(e->rank) * shard_amps : 0;
     if (p->input_amps) {
-      CK(cudaMemcpyAsync(psi, p->input_amps + first_amp, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
+      if (!input_copied)
+        CK(cudaMemcpyAsync(psi, p->input_amps + first_amp, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
       h2d += amps * sizeof(double2);
     } else {
       CK(cudaMemsetAsync(psi, 0, amps * sizeof(double2), s));

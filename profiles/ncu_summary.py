@@ -47,20 +47,26 @@ def main():
         print("  stalls per issued instruction:", ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:8]))
     if "--sass" in sys.argv:
         rows = ncu_csv(rep, "--page", "source", "--print-source", "sass")
-        h = rows[1]
-        iS, iE, iSrc = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("Source")
-        samp, ex = collections.Counter(), collections.Counter()
-        for row in rows[2:]:
-            toks = row[iSrc].split()
-            if not toks:
-                continue
-            op = (toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]).split(".")[0]
-            samp[op] += int(row[iS] or 0)
-            ex[op] += int(row[iE] or 0)
-        ts, te = sum(samp.values()) or 1, sum(ex.values()) or 1
-        print(f"  SASS mix (executed warp-instructions {te}):")
-        for op, s in samp.most_common(14):
-            print(f"    {op:8s} samples {100 * s / ts:5.1f}%  executed {100 * ex[op] / te:5.1f}%")
+        # one section per kernel: a "Kernel Name" row, a header row, instruction rows
+        starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] or [0]
+        for si, st0 in enumerate(starts):
+            end = starts[si + 1] if si + 1 < len(starts) else len(rows)
+            h = rows[st0 + 1]
+            iS, iE, iSrc = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("Source")
+            samp, ex = collections.Counter(), collections.Counter()
+            for row in rows[st0 + 2:end]:
+                if len(row) != len(h):
+                    continue
+                toks = row[iSrc].split()
+                if not toks:
+                    continue
+                op = (toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]).split(".")[0]
+                samp[op] += int(row[iS] or 0)
+                ex[op] += int(row[iE] or 0)
+            ts, te = sum(samp.values()) or 1, sum(ex.values()) or 1
+            print(f"  kernel {si}: SASS mix (executed warp-instructions {te}):")
+            for op, s_ in samp.most_common(14):
+                print(f"    {op:8s} samples {100 * s_ / ts:5.1f}%  executed {100 * ex[op] / te:5.1f}%")
 
 
 if __name__ == "__main__":
