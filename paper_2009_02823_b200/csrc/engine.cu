@@ -30,6 +30,7 @@
 
 #include "../../include/svgrad_b200.h"
 #include "device.cuh"
+#include "hash128.h"
 #include "jit.h"
 #include "kernels.h"
 #include "nccl_shim.h"
@@ -208,8 +209,9 @@ struct svg_engine {
   // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
   mutable std::map<std::tuple<int, int, int, size_t>, int> occ_memo;
   // segment plans are pure functions of a pass's flip / touch / dense pattern
-  mutable std::unordered_map<std::string, std::vector<Segment>> seg_memo;
-  mutable std::unordered_map<std::string, std::pair<std::vector<Step>, std::vector<int>>> plan_memo;  // why auto mode fell back to the interpreted kernels
+  mutable std::unordered_map<Key128, std::vector<Segment>, Key128Hash> seg_memo;
+  mutable std::unordered_map<Key128, std::pair<std::shared_ptr<const std::vector<Segment>>, Swizzle>, Key128Hash> choice_memo;
+  mutable std::unordered_map<Key128, std::shared_ptr<const std::pair<std::vector<Step>, std::vector<int>>>, Key128Hash> plan_memo;  // why auto mode fell back to the interpreted kernels
   DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
   HostBuf hblob, hres;
   // sharding: the state is split over 2^shard_bits shards by its top physical
@@ -602,18 +604,18 @@ bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
 std::vector<Segment> memo_segments(const svg_engine* e, const std::vector<uint32_t>& flips,
                                    const std::vector<uint32_t>& touch, const std::vector<char>& dense, int k,
                                    int regbits, bool free = false) {
-  std::string key;
-  key.reserve(12 + flips.size() * 9);
-  const int32_t head[] = {k, regbits, free ? 1 : 0};
-  key.append(reinterpret_cast<const char*>(head), sizeof(head));
-  key.append(reinterpret_cast<const char*>(flips.data()), flips.size() * 4);
-  key.append(reinterpret_cast<const char*>(touch.data()), touch.size() * 4);
-  key.append(dense.data(), dense.size());
+  Hasher h;
+  const int32_t head[] = {k, regbits, free ? 1 : 0, static_cast<int32_t>(flips.size())};
+  h.pod(head);
+  h.bytes(flips.data(), flips.size() * 4);
+  h.bytes(touch.data(), touch.size() * 4);
+  h.bytes(dense.data(), dense.size());
+  const Key128 key = h.key();
   auto it = e->seg_memo.find(key);
   if (it != e->seg_memo.end()) return it->second;
   std::vector<Segment> segs = free ? plan_segments_free(flips, touch, k, regbits) : plan_segments(flips, touch, dense, k, regbits);
   if (e->seg_memo.size() > 16384) e->seg_memo.clear();
-  e->seg_memo.emplace(std::move(key), segs);
+  e->seg_memo.emplace(key, segs);
   return segs;
 }
 
@@ -697,28 +699,30 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   std::vector<int> l2p_final;
   // the schedule is a pure function of the gate shapes and plan parameters: memoised
   auto schedule = [&](const PlanParams& pq, std::vector<int>* l2p_out) {
-    std::string key;
-    key.reserve(32 + logical.size() * sizeof(GateShape));
-    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs};
-    key.append(reinterpret_cast<const char*>(head), sizeof(head));
+    Hasher h;
+    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs, static_cast<int32_t>(logical.size())};
+    h.pod(head);
     for (const GateShape& sh : logical) {
-      key.append(reinterpret_cast<const char*>(&sh.flip), 8);
-      key.append(reinterpret_cast<const char*>(&sh.touch), 8);
-      key.append(reinterpret_cast<const char*>(&sh.nderiv), 4);
+      h.word(sh.flip);
+      h.word(sh.touch);
+      h.word(static_cast<uint64_t>(sh.nderiv));
     }
+    const Key128 key = h.key();
     auto it = e->plan_memo.find(key);
     if (it != e->plan_memo.end()) {
-      if (l2p_out) *l2p_out = it->second.second;
-      return it->second.first;
+      if (l2p_out) *l2p_out = it->second->second;
+      return it->second;
     }
     std::vector<int> l2p;
     std::vector<Step> st = plan_schedule(logical, n, g, pq, &l2p);
+    auto entry = std::make_shared<const std::pair<std::vector<Step>, std::vector<int>>>(std::move(st), std::move(l2p));
     if (e->plan_memo.size() > 64) e->plan_memo.clear();
-    e->plan_memo.emplace(std::move(key), std::make_pair(st, l2p));
-    if (l2p_out) *l2p_out = l2p;
-    return st;
+    e->plan_memo.emplace(key, entry);
+    if (l2p_out) *l2p_out = entry->second;
+    return std::shared_ptr<const std::pair<std::vector<Step>, std::vector<int>>>(entry);
   };
-  const std::vector<Step> steps = schedule(pp, &l2p_final);
+  const auto sched = schedule(pp, &l2p_final);
+  const std::vector<Step>& steps = sched->first;
   // free-lane plans and carried scales need the generated kernels (the
   // interpreter keeps lanes on tile positions 0..4)
   const bool jit_planned = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) &&
@@ -728,7 +732,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // kernels) it runs its own schedule over larger tiles -- one buffer per tile
   // leaves room for 2^(k+1) amplitudes per CTA: fewer HBM passes.
   int kf = L.k;
-  std::vector<Step> steps_fsplit;
+  std::shared_ptr<const std::pair<std::vector<Step>, std::vector<int>>> sched_f;
   // (auto: states of >= kFwdSplitQubits qubits, whose passes stream HBM; smaller,
   // L2-resident states are better served by more, smaller tiles -- measured cfg 2)
   if (g == 0 && jit_planned && nloc > L.k && (e->opt_tile_fwd > 0 || (e->opt_tile_fwd == 0 && nloc >= kFwdSplitQubits))) {
@@ -737,12 +741,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     if (kf > L.k) {
       PlanParams pq = pp;
       pq.k = kf;
-      steps_fsplit = schedule(pq, nullptr);
+      sched_f = schedule(pq, nullptr);
     } else {
       kf = L.k;
     }
   }
-  const std::vector<Step>& fsteps = kf > L.k ? steps_fsplit : steps;
+  const std::vector<Step>& fsteps = kf > L.k ? sched_f->first : steps;
   // physical gates per pass step, parallel to the step's items
   std::vector<GateList> pgates(steps.size());
   std::deque<svg_gate> pstore;  // remapped copies (only when the qubit map is not the identity)
@@ -784,7 +788,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   SVGB_PHASE(2);
   // segments per pass (register path)
-  std::vector<std::vector<Segment>> psegs(steps.size()), psegs_f(fsteps.size());
+  using SegsPtr = std::shared_ptr<const std::vector<Segment>>;
+  std::vector<SegsPtr> psegs(steps.size()), psegs_f(fsteps.size());
   std::vector<Swizzle> pswz(steps.size()), pswz_f(fsteps.size());
   // free-lane plans also need tile staging (a first segment off the global
   // layout reads its tile from the staged copy)
@@ -793,7 +798,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // plan, or the free-lane plan when the cost model prefers it (lc: lane op,
   // xc: layout change, in register-op units)
   auto pass_segments = [&](const Pass& ps, const GateList& gl, const std::vector<GateShape>& shp, int kk, int R,
-                           double lc, double xc, std::vector<Segment>* out, Swizzle* swz) {
+                           double lc, double xc, SegsPtr* outp, Swizzle* swz) {
     const TileMap tm = tile_map(ps.qmask);
     std::vector<uint32_t> flips(ps.items.size()), touch(ps.items.size());
     std::vector<char> dense(ps.items.size());
@@ -802,7 +807,25 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       touch[j] = tm.local(shp[j].touch);
       dense[j] = !reg_capable(gl[j], flips[j]);
     }
-    *out = memo_segments(e, flips, touch, dense, kk, R);
+    // the choice (plan + swizzle) is memoised per pass structure and cost model
+    Hasher h;
+    const int32_t head[] = {kk, R, free_lanes ? 1 : 0, static_cast<int32_t>(flips.size())};
+    h.pod(head);
+    h.pod(lc);
+    h.pod(xc);
+    h.bytes(flips.data(), flips.size() * 4);
+    h.bytes(touch.data(), touch.size() * 4);
+    h.bytes(dense.data(), dense.size());
+    const Key128 ck = h.key();
+    auto hit = e->choice_memo.find(ck);
+    if (hit != e->choice_memo.end()) {
+      *outp = hit->second.first;
+      *swz = hit->second.second;
+      for (const Segment& sg : **outp) L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
+      return;
+    }
+    auto chosen = std::make_shared<std::vector<Segment>>(memo_segments(e, flips, touch, dense, kk, R));
+    std::vector<Segment>* out = chosen.get();
     bool free_ok = free_lanes;
     for (size_t j = 0; j < ps.items.size() && free_ok; ++j) free_ok = !dense[j] && __builtin_popcount(flips[j]) <= 1;
     if (free_ok) {
@@ -815,6 +838,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       L.free_lanes_used = L.free_lanes_used || sg.lanemask != 31u;
     }
     *swz = choose_swizzle(ls, kk);
+    *outp = chosen;
+    if (e->choice_memo.size() > 16384) e->choice_memo.clear();
+    e->choice_memo.emplace(ck, std::make_pair(*outp, *swz));
   };
   if (L.reg) {
     // register-op units per amplitude: a lane flip is a warp shuffle of both (fwd:
@@ -881,14 +907,14 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       l.swz = pswz_f[si];
       uint32_t prev = ~0u, prev_l = ~0u;
       double C = 1.0;  // deferred scale; flushed when the layout changes (see SegDesc.scale)
-      for (const Segment& sg : psegs_f[si]) {
+      for (const Segment& sg : *psegs_f[si]) {
         SegLocal sl;
         SegDesc sd = make_seg(sg.reg ? SEG_REG : SEG_SMEM, sg.reg ? sg.regmask : default_regs(RF),
                               sg.reg ? sg.lanemask : 31u, l.swz, kf, RF, &sl);
         sd.same_map = sg.reg && sg.regmask == prev && sg.lanemask == prev_l;
         prev = sg.reg ? sg.regmask : ~0u;
         prev_l = sg.reg ? sg.lanemask : ~0u;
-        if (!sd.same_map && !(carry && all_reg(psegs_f[si]))) C = 1.0;
+        if (!sd.same_map && !(carry && all_reg(*psegs_f[si]))) C = 1.0;
         if (sg.reg) {
           sd.op_begin = static_cast<int>(L.rops.size());
           for (int it : sg.items) emit_rop(L, tm, sl, gs[it], ROP_FWD, gs[it].fwd, nullptr, 0, real_sums, &C);
@@ -912,7 +938,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       }
       l.d.seg_end = static_cast<int>(L.segs.size());
       l.d.op_end = static_cast<int>(L.rops.size());
-      if (psegs_f[si].size() > 1) l.tiles = true;
+      if (psegs_f[si]->size() > 1) l.tiles = true;
       L.fwd.push_back(l);
     }
     L.pass_bytes += 2 * S;
@@ -1030,7 +1056,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       } else {
         Launch l = reg_launch(ps, 2, L.k);
         l.swz = pswz[si];
-        const std::vector<Segment>& sgs = psegs[si];
+        const std::vector<Segment>& sgs = *psegs[si];
         uint32_t prev = ~0u, prev_l = ~0u;
         double C = 1.0;
         for (auto st = sgs.rbegin(); st != sgs.rend(); ++st) {
