@@ -106,8 +106,8 @@ def load(path: str = LIB_PATH):
         lib.svg_engine_destroy.argtypes = [C.c_void_p]
         lib.svg_engine_set_stream.argtypes = [C.c_void_p, C.c_void_p]
         lib.svg_engine_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
-        lib.svg_reverse_sweep.argtypes = [
-            C.c_void_p, C.POINTER(svg_problem), C.POINTER(c128), C.POINTER(c128),
+        lib.svg_reverse_sweep.argtypes = [  # sums / derivs: complex128 buffers (numpy-owned)
+            C.c_void_p, C.POINTER(svg_problem), C.c_void_p, C.c_void_p,
             C.POINTER(c128), C.POINTER(svg_stats),
         ]
         lib.svg_expectation.argtypes = [C.c_void_p, C.POINTER(svg_problem), C.POINTER(c128), C.POINTER(svg_stats)]
@@ -178,14 +178,17 @@ class Engine:
         check(self.lib.svg_engine_set_stream(self.handle, C.c_void_p(stream_ptr or None)))
 
     def reverse_sweep(self, problem: svg_problem, num_params: int, num_derivs: int):
-        sums = (c128 * max(1, num_params))()
-        derivs = (c128 * max(1, num_derivs))()
+        """(sums complex128[P], derivs complex128[D], energy, stats) of one sweep."""
+        import numpy as np
+
+        sums = np.zeros(max(1, num_params), dtype=np.complex128)
+        derivs = np.zeros(max(1, num_derivs), dtype=np.complex128)
         energy = c128()
         stats = svg_stats()
         with self.lock:
-            check(self.lib.svg_reverse_sweep(self.handle, C.byref(problem), sums, derivs,
+            check(self.lib.svg_reverse_sweep(self.handle, C.byref(problem), sums.ctypes.data, derivs.ctypes.data,
                                              C.byref(energy), C.byref(stats)))
-        return sums, derivs, energy, stats
+        return sums[:num_params], derivs[:num_derivs], energy, stats
 
     def expectation(self, problem: svg_problem):
         energy = c128()

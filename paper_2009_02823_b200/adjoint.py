@@ -101,7 +101,7 @@ def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, s
     eng = engine or _native.engine(device)
     sums, _, energy, st = eng.reverse_sweep(problem.c, circuit.num_params, problem.num_derivs)
     _account(counters, audit, len(circuit.gates), problem.num_derivs)
-    out = np.ctypeslib.as_array(sums).view(np.complex128)[: circuit.num_params].copy()
+    out = sums
     if stats is not None:
         stats.update(st.as_dict())
     return out, complex(energy.re, energy.im)

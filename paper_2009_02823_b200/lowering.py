@@ -35,7 +35,7 @@ from . import _native as N
 from .ir import NonInvertibleGateError, SIGMA, bound_matrix, derivative_scale, invert_small, kind_name, matrix_derivative
 from .operators import pauli_masks, pauli_strings
 
-GATE_DTYPE = np.dtype(
+GATE_DTYPE = np.dtype(  # itemsize 816 = 51 complex128 slots (bind scatters into a flat complex view)
     [
         ("form", "<i4"), ("ntargets", "<i4"), ("targets", "<i4", (2,)), ("ctrl_mask", "<u8"),
         ("x_mask", "<u8"), ("z_mask", "<u8"), ("n_y", "<i4"), ("nderiv", "<i4"),
@@ -155,22 +155,26 @@ def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     if hit is None or hit[0] is not st:
         if len(tls) > 16:
             tls.clear()
-        hit = tls[id(st)] = (st, st.gates.copy(), st.derivs.copy())
-    gates, derivs = hit[1], hit[2]
+        g, d = st.gates.copy(), st.derivs.copy()
+        # the rotation coefficients a, b of (fwd, rewind, adjoint) as positions in a
+        # flat complex view of the gate records: one scatter per call
+        flat = g.view(np.complex128).reshape(-1)
+        rec = GATE_DTYPE.itemsize // 16
+        base = st.rot_gates * rec
+        pos = np.concatenate([base + (GATE_DTYPE.fields[f][1] // 16) + j
+                              for f in ("fwd", "rewind", "adjoint") for j in (0, 1)])
+        hit = tls[id(st)] = (st, g, d, flat, pos, d["k"], d["basis"])
+    gates, derivs, flat, pos, dk, dbasis = hit[1:]
     scale = derivative_scale()
     if st.rot_gates.size:
         ang = st.rot_alpha * params[st.rot_refs]
         a = np.cos(ang) + 0j
         b = 1j * np.sin(ang)
-        gates["fwd"][st.rot_gates, 0] = a
-        gates["fwd"][st.rot_gates, 1] = b
-        gates["rewind"][st.rot_gates, 0] = np.conj(a)
-        gates["rewind"][st.rot_gates, 1] = np.conj(b)
-        gates["adjoint"][st.rot_gates, 0] = np.conj(a)
-        gates["adjoint"][st.rot_gates, 1] = np.conj(b)
+        ca, cb = np.conj(a), np.conj(b)
+        flat[pos] = np.concatenate((a, b, ca, cb, ca, cb))  # fwd, rewind, adjoint
         # post-gate generator (basis 1): dU phi_i = alpha*i P U phi_i = alpha*i P phi_{i+1}
-        derivs["k"][st.rot_derivs, 1] = (st.rot_alpha * 1j) * scale
-        derivs["basis"][st.rot_derivs] = 1
+        dk[st.rot_derivs, 1] = (st.rot_alpha * 1j) * scale
+        dbasis[st.rot_derivs] = 1
     if st.fixed_pauli.size:
         for field in ("fwd", "rewind", "adjoint"):
             gates[field][st.fixed_pauli, 1] = 1.0
