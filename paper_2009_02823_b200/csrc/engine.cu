@@ -473,8 +473,9 @@ constexpr int kJitMinQubits = 18;
 // Gates per register-tile pass: beyond ~40 the straight-line pass kernels
 // outgrow the instruction cache (measured: cfg 3 reverse 115 ms at 96, 105 ms at 40).
 constexpr int kRegPassGates = 40;
-// Forward sweeps of states this large run their own schedule over k+1-qubit tiles.
-constexpr int kFwdSplitQubits = 24;
+// States this large (per shard) stream HBM: generated kernels use 12-qubit tiles
+// (a narrower reverse tile gets a forward schedule over k+1-qubit tiles).
+constexpr int kWideTileQubits = 24;
 
 // One register op for gate g: operator coefficients `c` (a, b of a I + b P),
 // optionally fused with the post-gate generator `kpost` into `slot`.
@@ -671,6 +672,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // (one CTA pair); wider tiles mean fewer passes (measured cfg 2: k 11 / R 4 6 % faster)
   const bool jit_expected = e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits);
   L.k = choose_tile_qubits(nloc, static_cast<int>(e->opt_tile), e->sms, jit_expected ? 2 : 4);
+  // HBM-resident states with generated kernels: 12-qubit tiles (one 256-thread CTA
+  // per SM; fewer passes -- measured cfg 3 reverse -7 %, cfg 4 -9 %)
+  if (e->opt_tile == 0 && jit_expected && nloc >= kWideTileQubits && (int64_t(1) << (nloc - 12)) >= 2ll * e->sms)
+    L.k = 12;
   L.b = (nloc <= L.k) ? nloc : std::min(5, L.k - 2);
   if (g > 0 && L.b < 5 && nloc > L.k) throw InvalidArg("sharded engines need >= 7 qubits per shard");
   // register bits (amplitudes per thread per buffer = 2^R): auto = 4 for the
@@ -681,7 +686,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   const int RB = e->opt_reg_bits ? static_cast<int>(e->opt_reg_bits) : Rauto;          // reverse passes
   const int RF = e->opt_reg_bits_fwd ? static_cast<int>(e->opt_reg_bits_fwd) : Rauto;  // forward passes
   L.R = RB;
-  auto fits = [&](int R) { return L.k - 5 - R >= 0 && (32 << (L.k - 5 - R)) <= reg_max_threads(R); };
+  // thread count of a register-tile CTA: the interpreter's launch bounds, or 512
+  // for the generated kernels (their launch bounds follow the thread count)
+  auto fits = [&](int R) {
+    return L.k - 5 - R >= 0 && (32 << (L.k - 5 - R)) <= (jit_expected ? 512 : reg_max_threads(R));
+  };
   L.reg = e->opt_kernel != 1 && L.b >= 5 && fits(RB) && fits(RF);
   if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 5 + reg_bits .. 13 tile qubits");
   PlanParams pp;
@@ -733,9 +742,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   // leaves room for 2^(k+1) amplitudes per CTA: fewer HBM passes.
   int kf = L.k;
   std::shared_ptr<const std::pair<std::vector<Step>, std::vector<int>>> sched_f;
-  // (auto: states of >= kFwdSplitQubits qubits, whose passes stream HBM; smaller,
+  // (auto: states of >= kWideTileQubits qubits, whose passes stream HBM; smaller,
   // L2-resident states are better served by more, smaller tiles -- measured cfg 2)
-  if (g == 0 && jit_planned && nloc > L.k && (e->opt_tile_fwd > 0 || (e->opt_tile_fwd == 0 && nloc >= kFwdSplitQubits))) {
+  if (g == 0 && jit_planned && nloc > L.k &&
+      (e->opt_tile_fwd > 0 || (e->opt_tile_fwd == 0 && nloc >= kWideTileQubits && L.k <= 11))) {
     kf = e->opt_tile_fwd > 0 ? static_cast<int>(e->opt_tile_fwd) : L.k + 1;
     kf = std::max(L.k, std::min({kf, nloc, 13}));
     if (kf > L.k) {
@@ -945,6 +955,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
   }
 
   SVGB_PHASE(4);
+  // observable passes keep 11-qubit tiles next to 12-qubit gate passes (their
+  // per-term work is light: more, smaller tiles balance better -- measured cfg 3)
+  PlanParams pp_obs = pp;
+  if (jit_planned && L.k == 12 && e->opt_tile == 0) pp_obs.k = 11;
+  const int kobs = pp_obs.k;
   // observable passes: terms in the final physical layout, grouped by the flip
   // pattern on rank bits (a nonzero pattern reads the partner shard's psi), then
   // by local flip mask into tiles
@@ -973,7 +988,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     std::vector<uint64_t> flips(members.size());
     for (size_t j = 0; j < members.size(); ++j) flips[j] = pterms[members[j]].x_mask & loc_mask;
     std::vector<int> direct;
-    std::vector<Pass> tpasses = plan_term_passes(flips, pp, &direct);
+    std::vector<Pass> tpasses = plan_term_passes(flips, pp_obs, &direct);
     if (!direct.empty()) {  // wide flip masks: one untiled gather pass (qmask 0)
       Pass ps;
       ps.items = direct;
@@ -988,7 +1003,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     for (const Pass& ps : tpasses) {
       const TileMap tm = tile_map(ps.qmask);
       Launch l;
-      l.d = make_desc(nloc, L.k, ps.qmask);
+      l.d = make_desc(nloc, kobs, ps.qmask);
       l.d.op_begin = static_cast<int>(L.terms.size());
       l.d.untiled = ps.qmask == 0;
       l.d.xglob = xg;
@@ -1114,7 +1129,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
 
   SVGB_PHASE(6);
   // grids, shared memory, partial offsets
-  auto ntiles_of = [&](const Launch& l) { return int64_t(1) << (nloc - (l.kind == L_REG ? l.d.k : L.k)); };
+  auto ntiles_of = [&](const Launch& l) {
+    return int64_t(1) << (nloc - ((l.kind == L_REG || l.kind == L_OBS) ? l.d.k : L.k));
+  };
   // lane-group inner-product accumulators: combine 2^shift lanes so that the
   // shared accumulators stay within 24 KB (two 128-thread CTAs with 64 KB of
   // transpose tiles still fit an SM; no per-op full warp reductions)
@@ -1182,11 +1199,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
             }
             l.jit->blocks_per_sm = blocks;
           }
-          l.grid = clamp_grid(l.jit->blocks_per_sm);
+          l.grid = clamp_grid_k(l.jit->blocks_per_sm, ntiles_of(l));
           break;
         }
-        l.smem = obs_smem(L.k, l.d.b, l.d.op_end - l.d.op_begin);
-        l.grid = clamp_grid(memo_occ(-3, 0, 0, l.smem, [&] { return occupancy(1, l.smem); }));
+        l.smem = obs_smem(l.d.k, l.d.b, l.d.op_end - l.d.op_begin);
+        l.grid = clamp_grid_k(memo_occ(-3, 0, 0, l.smem, [&] { return occupancy(1, l.smem); }), ntiles_of(l));
         break;
       case L_OBS_DIRECT:
         l.smem = 0;
@@ -1215,7 +1232,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
         // minus tile / staging buffers and per-warp accumulators.  Every halving
         // of the accumulators costs a butterfly step per op (measured: 40-slot
         // passes 8 % slower at shift 1 than at shift 0).
-        const int blocks = l->nb == 2 ? (e->opt_jit_blocks_rev ? int(e->opt_jit_blocks_rev) : 2)
+        const int blocks = l->nb == 2 ? (e->opt_jit_blocks_rev ? int(e->opt_jit_blocks_rev) : std::max(1, std::min(2, 256 / l->threads)))
                                       : (e->opt_jit_blocks_fwd ? int(e->opt_jit_blocks_fwd) : (l->R == 3 ? 2 : 4));
         const size_t share = std::min<size_t>(e->max_smem, (size_t(e->max_smem_sm) / blocks) - 1024);
         const size_t fixed = (sizeof(double2) << l->d.k) * l->nb + sizeof(double2) * (l->threads / 32) * l->d.nslots;
@@ -1259,7 +1276,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
       for (Launch& l : L.obs) {
         if (l.kind != L_OBS) continue;
         JitObsPass op;
-        op.k = L.k;
+        op.k = l.d.k;
         op.b = l.d.b;
         op.nloc = nloc;
         op.threads = kThreads;
