@@ -16,6 +16,10 @@ passes, finalize) of the configured circuit.  Rank 0 prints ONE JSON line.
 * ``roofline``: the dominant kernel (k_rev_pass, the fused reverse pass):
   algorithmic bytes per launch = 4 * S (read+write phi and lambda, S = 16*2^n)
   over its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs.
+* ``roofline_fp64``: the reverse sweep's algorithmic FP64 work (6 FMA per
+  amplitude per parametrised gate) over its device time, against the DFMA peak
+  measured on B200 (the reverse passes are FP64-bound above ~16 gates per pass,
+  profiles/README.md "pass cost model").
 * ``cpu_baseline``: the C restatement of the reference's schedule
   (oracle/, "port") on the host cores, bounded sample (rank 0, N=1).
 * ``--impl reference``: that same CPU port as the reference arm.
@@ -32,6 +36,8 @@ Multi-GPU (torchrun, N>1), max-over-ranks device time:
   sums), ``scaling: "strong"``, value = gradients of the whole job / time.
 """
 from __future__ import annotations
+
+FP64_PEAK_TFLOPS = 37.17  # B200 DFMA peak measured here (tools/ubench/peaks.cu, 32 warps/SM)
 
 import argparse
 import json
@@ -310,6 +316,7 @@ def run_ours(args, rank, world, local_rank):
     traffic = _traffic_per_launch(f"cfg{args.config}") if args.qubits is None and world == 1 else None
     value = jobs * args.steps / (total_ms * 1e-3)
     B_alg = 6 * w.num_gates * S  # gate-level algorithmic bytes per gradient
+    n_param_gates = sum(1 for g in w.circuit.gates if len(g.param_refs) > 0)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cval, cores, reps, secs = _cpu_port(w, sv.init_basis_state(n))
@@ -334,6 +341,18 @@ def run_ours(args, rank, world, local_rank):
             "bytes_per_launch": 4 * S_rank,
             "avg_launch_ms": avg_launch_ms, "peak_source": peak_src,
         },
+        # the reverse sweep is FP64-bound above ~16 gates per pass: its algorithmic
+        # FP64 work is 6 FMA (12 flop) per amplitude per parametrised gate (rewind
+        # phi and lambda: 2 FMA each, Re<lambda|K|phi>: 2), against the DFMA peak
+        # measured with tools/ubench/peaks.cu (profiles/r01_ubench_peaks.jsonl)
+        "roofline_fp64": {
+            "kernel": "reverse sweep (all reverse passes)", "unit": "TFLOP/s",
+            "flop_per_gradient": 12 * (S_rank // 16) * n_param_gates,
+            "achieved": 12 * (S_rank // 16) * n_param_gates / (phases["reverse"] * 1e-3) / 1e12,
+            "peak": FP64_PEAK_TFLOPS,
+            "frac": 12 * (S_rank // 16) * n_param_gates / (phases["reverse"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+            "peak_source": "measured DFMA throughput, tools/ubench/peaks.cu (37.2 TFLOP/s at 1965 MHz)",
+        } if phases.get("reverse") else None,
         "phase_ms": {k: round(v, 4) for k, v in phases.items()},
         "passes": {"forward": int(st_last["fwd_passes"]), "observable": int(st_last["obs_passes"]),
                    "reverse": int(st_last["rev_passes"])},
