@@ -49,6 +49,40 @@ def test_gpu_matches_reference_golden_large(name):
     assert vars(rep.counters) == gold["counters"]
 
 
+_VARIANTS = {  # generated-kernel plan options (engine defaults: all on / auto)
+    "wide_tiles": {"tile_qubits": 12, "tile_fwd": -1},
+    "wide_tiles_fixed_lanes": {"tile_qubits": 12, "free_lanes": 0},
+    "fwd_split_13": {"tile_qubits": 12, "tile_fwd": 13},
+    "fwd_split_12": {"tile_qubits": 11, "tile_fwd": 12},
+    "no_scale_carry": {"scale_carry": 0},
+    "no_fused_diag": {"fuse_diag": 0},
+    "no_acc_prefetch_acc8": {"acc_prefetch": 0, "acc_kb": 8},
+    "lane_cost_low": {"lane_cost10": 10},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(_VARIANTS))
+@pytest.mark.parametrize("name", ["cfg3_n20", "cfg5_n20"])
+def test_generated_kernel_variants_match_reference_golden(name, variant):
+    """Every plan / code-generation option of the generated kernels (free-lane
+    layouts, swizzled transposes, 12-qubit tiles, separate forward schedules,
+    carried scales, fused diagonal runs, accumulator modes) against the golden."""
+    gold = load_golden(f"golden_{name}.json")[name]
+    circ, theta, obs, inp, method = materialize(large_config_cases()[name])
+    opts = {"jit": 2, **_VARIANTS[variant]}
+    eng = sv._native.engine()
+    try:
+        for k, v in opts.items():
+            eng.set_option(k, v)
+        rep = _run(circ, theta, obs, inp, method)
+    finally:
+        for k, v in {"jit": 1, "tile_qubits": 0, "tile_fwd": 0, "free_lanes": 1, "scale_carry": 1, "fuse_diag": 1,
+                     "acc_prefetch": 1, "acc_kb": 0, "lane_cost10": 37}.items():
+            eng.set_option(k, v)
+    assert max_err(rep.values, cvec(gold["values"])) <= GRAD_TOL
+    assert abs(rep.energy - complex(*gold["energy"])) <= ENERGY_TOL
+
+
 @pytest.mark.parametrize("tile", [0, 7, 8, 9, 11, 12])
 def test_tile_size_invariance(tile):
     """Different pass plans (tile widths) reorder commuting gates only."""

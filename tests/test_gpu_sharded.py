@@ -132,6 +132,23 @@ def test_virtual_shards_match_single_shard_midsize(cfg, n, shards):
     assert abs(rep.energy - ref.energy) <= ENERGY_TOL
 
 
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_sharded_wide_tiles_match_single_shard(cfg):
+    """Shards of >= 24 qubits: 12-qubit tiles, free-lane layouts and carried scales in
+    the generated kernels, with swaps through the NCCL data path (emulated)."""
+    n = 25
+    w = sv.build_workload(cfg, n)
+    inp = sv.BasisState(n)
+    ref = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp)
+    eng = sv.distributed.virtual_engine(2)
+    eng.set_option("emulate_transport", 1)
+    stats = {}
+    rep = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp, engine=eng, stats=stats)
+    assert stats["tile_qubits"] == 12 and stats["jit_passes"] > 0
+    assert max_err(rep.values, ref.values) <= GRAD_TOL
+    assert abs(rep.energy - ref.energy) <= ENERGY_TOL
+
+
 def test_virtual_shards_expectation_and_determinism():
     circ, theta, obs, inp, _ = materialize(SMALL["cfg5_n15"])
     eng = _engine(4)
