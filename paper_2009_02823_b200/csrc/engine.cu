@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <deque>
 #include <map>
 #include <unordered_map>
@@ -152,6 +153,7 @@ struct Lowered {
   int64_t swap_bytes = 0;  // bytes each shard exchanges (swaps both ways + partner fetches)
   bool reg = false;  // register-tile kernels in use
   bool free_lanes_used = false;  // some pass has a segment off the global lane layout (generated kernels only)
+  bool fwd_early = false;        // forward launches handed to lower()'s fwd_ready callback (already launched)
   bool jit_planned = false;      // register passes planned for the generated kernels (deferred scale carried
                                  // across layout changes, see JitPass.scale_carry)
   int R = 3;         // their register bits
@@ -197,6 +199,7 @@ struct svg_engine {
   int64_t opt_free_lanes = 1;    // generated kernels: free-lane segment plans where cheaper
   int64_t opt_scale_carry = 1;   // generated kernels: deferred scale carried across layout changes
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
+  int64_t opt_early_fwd = 1;     // one shard: launch the forward passes while the rest is lowered
   int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
@@ -222,6 +225,7 @@ struct svg_engine {
   int rank = 0;
   NcclComm comm = nullptr;
   cudaEvent_t ev[6] = {};
+  cudaEvent_t blob_ev = nullptr;  // the last table upload from the pinned staging buffer
 };
 
 namespace {
@@ -658,7 +662,11 @@ thread_local std::chrono::steady_clock::time_point g_phase_t;
     g_phase_t = now_;                                                                                  \
   } while (0)
 
-Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
+// fwd_ready (optional): called once the forward launches are complete and sized
+// -- generated kernels only, no shared-memory segments -- so the caller can start
+// them while the rest (observable, reverse sweep) is still being lowered.
+Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
+              const std::function<void(Lowered&)>& fwd_ready = {}) {
   g_phase_t = std::chrono::steady_clock::now();
   Lowered L;
   const int n = p->num_qubits;
@@ -954,6 +962,60 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     L.pass_bytes += 2 * S;
   }
 
+  // Early forward launches: generated kernels with register segments only need
+  // no device tables (their coefficients travel in the launch parameters).
+  if (fwd_ready && jit_planned && !e->jit_dry_run && !L.fwd.empty()) {
+    bool ok = true;
+    for (const Launch& l : L.fwd) {
+      ok = ok && l.kind == L_REG;
+      for (int si = l.d.seg_begin; ok && si < l.d.seg_end; ++si) ok = L.segs[si].kind == SEG_REG;
+    }
+    if (ok) {
+      std::vector<JitPass> passes;
+      for (Launch& l : L.fwd) {
+        JitPass jp;
+        jp.R = l.R;
+        jp.nb = 1;
+        jp.k = l.d.k;
+        jp.nloc = nloc;
+        jp.threads = l.threads;
+        jp.tiles = l.tiles;
+        jp.stage = e->opt_stage != 0;
+        jp.fuse_diag = e->opt_fuse_diag != 0;
+        jp.acc_prefetch = e->opt_acc_prefetch != 0;
+        jp.min_blocks = static_cast<int>(e->opt_jit_blocks_fwd);
+        jp.rest = l.d.rest;
+        jp.q = l.d.q;
+        jp.swz = l.swz.col;
+        jp.scale_carry = carry;
+        jp.segs = L.segs.data() + l.d.seg_begin;
+        jp.nsegs = l.d.seg_end - l.d.seg_begin;
+        jp.rops = L.rops.data() + l.d.op_begin;
+        jp.op_begin = l.d.op_begin;
+        passes.push_back(jp);
+      }
+      std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->device);
+      for (size_t i = 0; i < ks.size(); ++i) {
+        Launch& l = L.fwd[i];
+        l.jit = ks[i];
+        l.smem = l.jit->smem;
+        if (l.jit->blocks_per_sm <= 0) {
+          int blocks = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, reinterpret_cast<const void*>(l.jit->fn),
+                                                            l.threads, l.smem) != cudaSuccess || blocks < 1) {
+            (void)cudaGetLastError();
+            blocks = 1;
+          }
+          l.jit->blocks_per_sm = blocks;
+        }
+        const int64_t nt = int64_t(1) << (nloc - l.d.k);
+        l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nt, int64_t(e->sms) * l.jit->blocks_per_sm)));
+      }
+      fwd_ready(L);
+      L.fwd_early = true;
+    }
+  }
+
   SVGB_PHASE(4);
   // observable passes keep 11-qubit tiles next to 12-qubit gate passes (their
   // per-term work is light: more, smaller tiles balance better -- measured cfg 3)
@@ -1222,7 +1284,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse) {
     std::vector<Launch*> regl;
     for (std::vector<Launch>* v : {&L.fwd, &L.rev})
       for (Launch& l : *v)
-        if (l.kind == L_REG) regl.push_back(&l);
+        if (l.kind == L_REG && !l.jit) regl.push_back(&l);
     std::vector<JitPass> passes;
     passes.reserve(regl.size());
     for (Launch* l : regl) {
@@ -1387,7 +1449,46 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
                          e->stream));
       input_copied = true;
     }
-    const Lowered L = lower(e, p, with_reverse);
+    // One shard: the initial state is set up before the lowering, and the forward
+    // passes go out as soon as they are lowered (lower()'s fwd_ready), so the GPU
+    // runs them while the host lowers the observable and the reverse sweep.
+    const bool early = e->shards_local == 1 && !e->comm && e->opt_early_fwd;
+    int64_t early_launches = 0;
+    std::function<void(Lowered&)> fwd_cb;
+    if (early) {
+      const size_t amps0 = size_t(1) << p->num_qubits;
+      e->psi.reserve(amps0 * sizeof(double2));
+      CK(cudaEventRecord(e->ev[0], e->stream));
+      if (!p->input_amps) {
+        CK(cudaMemsetAsync(e->psi.ptr, 0, amps0 * sizeof(double2), e->stream));
+        launch_set_basis(static_cast<double2*>(e->psi.ptr), static_cast<uint64_t>(p->input_basis), e->stream);
+        ++early_launches;
+      }
+      CK(cudaEventRecord(e->ev[1], e->stream));
+      fwd_cb = [&](Lowered& Lf) {
+        double2* psi0 = static_cast<double2*>(e->psi.ptr);
+        for (const Launch& l : Lf.fwd) {
+          const JitArgsHead head{psi0, nullptr, nullptr, nullptr, nullptr, l.d.part_off, 0};
+          std::vector<unsigned char> args =
+              jit_args(*l.jit, head, Lf.segs.data() + l.d.seg_begin, Lf.rops.data() + l.d.op_begin);
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(l.grid);
+          cfg.blockDim = dim3(l.threads);
+          cfg.dynamicSmemBytes = l.smem;
+          cfg.stream = e->stream;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          attr[0].val.programmaticStreamSerializationAllowed = e->opt_pdl ? 1 : 0;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          void* params[] = {args.data()};
+          CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(l.jit->fn), params));
+          ++early_launches;
+        }
+        CK(cudaEventRecord(e->ev[2], e->stream));
+      };
+    }
+    const Lowered L = lower(e, p, with_reverse, fwd_cb);
     const auto t_lowered = std::chrono::steady_clock::now();
     const int nloc = L.nloc;
     const int nsh = e->shards_local;       // shards held by this engine
@@ -1414,8 +1515,9 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
 
     char* hb = static_cast<char*>(e->hblob.ptr);
     char* db = static_cast<char*>(e->blob.ptr);
-    // the pinned staging buffer may still feed a previous call's copy
-    CK(cudaStreamSynchronize(s));
+    // the pinned staging buffer may still feed a previous call's copy (its event;
+    // a full stream sync would also wait for this call's early forward passes)
+    if (e->blob_ev) CK(cudaEventSynchronize(e->blob_ev));
     std::memcpy(hb + bl.ops, L.ops.data(), L.ops.size() * sizeof(DevOp));
     std::memcpy(hb + bl.coef, L.coef.data(), L.coef.size() * sizeof(double2));
     std::memcpy(hb + bl.terms, L.terms.data(), L.terms.size() * sizeof(DevTerm));
@@ -1511,15 +1613,18 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     };
     int64_t launches = 0, h2d = bl.total, d2h = 0;
     const auto t_launch = std::chrono::steady_clock::now();
-    CK(cudaEventRecord(e->ev[0], s));
+    const bool init_done = early;  // psi initialised before the lowering (ev[0], ev[1] recorded)
+    if (!init_done) CK(cudaEventRecord(e->ev[0], s));
     CK(cudaMemcpyAsync(db, hb, bl.total, cudaMemcpyHostToDevice, s));
+    if (!e->blob_ev) CK(cudaEventCreateWithFlags(&e->blob_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(e->blob_ev, s));
     // input: shards are consecutive slices of the full index range (identity layout at the start)
     const size_t first_amp = e->comm ? size_t(e->rank) * shard_amps : 0;
     if (p->input_amps) {
       if (!input_copied)
         CK(cudaMemcpyAsync(psi, p->input_amps + first_amp, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
       h2d += amps * sizeof(double2);
-    } else {
+    } else if (!init_done) {
       CK(cudaMemsetAsync(psi, 0, amps * sizeof(double2), s));
       const uint64_t idx = static_cast<uint64_t>(p->input_basis);
       if (idx >= first_amp && idx < first_amp + amps) {
@@ -1527,8 +1632,10 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         launches += 1;
       }
     }
-    CK(cudaEventRecord(e->ev[1], s));
+    launches += early_launches;
+    if (!init_done) CK(cudaEventRecord(e->ev[1], s));
     for (const Launch& l : L.fwd) {
+      if (L.fwd_early) break;  // launched by the fwd_ready callback
       if (l.kind == L_SWAP) {
         swap_buffer(psi, l.gbit, l.lpos);
         continue;
@@ -1544,7 +1651,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         ++launches;
       }
     }
-    CK(cudaEventRecord(e->ev[2], s));
+    if (!L.fwd_early) CK(cudaEventRecord(e->ev[2], s));
     for (const Launch& l : L.obs) {
       if (l.kind == L_FETCH) {
         if (e->comm) fetch_partner(l.d.xglob);
@@ -1799,6 +1906,7 @@ int svg_engine_destroy(svg_engine* e) {
   e->hres.release();
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
+  if (e->blob_ev) cudaEventDestroy(e->blob_ev);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
   delete e;
   return SVG_OK;
@@ -1837,6 +1945,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "lane_cost10" || k == "xpose_cost10") {
     if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
     (k == "lane_cost10" ? e->opt_lane_cost10 : e->opt_xpose_cost10) = value;
+  } else if (k == "early_fwd") {
+    e->opt_early_fwd = value != 0;
   } else if (k == "tile_fwd") {
     if (value < -1 || value > 13) return fail(SVG_EINVAL, "tile_fwd must be in [-1, 13]");
     e->opt_tile_fwd = value;

@@ -1,0 +1,13 @@
+o=gpurun_out/r24; mkdir -p $o
+run() { tag=$1; shift; timeout 300 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e "$@" > $o/$tag.json 2> $o/$tag.err; python - $o/$tag.json $tag <<'PY'
+import json,sys
+try:
+  d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(sys.argv[2], round(d['ms_per_step'],3), d['phase_ms'], d['passes'], d['config']['tile_qubits'])
+except Exception as e: print(sys.argv[2], 'fail', e)
+PY
+}
+run c2 --config 2 --steps 20 --warmup 5
+run c2t12 --config 2 --steps 20 --warmup 5 --tile-qubits 12
+run c2t12mg56 --config 2 --steps 20 --warmup 5 --tile-qubits 12 --max-gates 56
+run c3t12 --config 3 --tile-qubits 12
+run c3t12f13 --config 3 --tile-qubits 12 --opt tile_fwd=13
