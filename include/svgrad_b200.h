@@ -166,7 +166,10 @@ int svg_engine_set_stream(svg_engine* e, void* stream);
    "reg_bits" / "reg_bits_fwd" (3 or 4: 2^bits amplitudes per thread in reverse / forward passes),
    "jit" (circuit-specialised register-tile kernels compiled at run time with NVRTC:
    0 off, 1 auto = shards of >= 18 qubits, 2 always), "emulate_transport" (virtual engines:
-   run the NCCL data path with device copies), "prefetch" (ignored). */
+   run the NCCL data path with device copies), "prefetch" (ignored); generated-kernel plan
+   options (defaults on / auto): "free_lanes", "lane_cost10", "xpose_cost10", "scale_carry",
+   "fuse_diag", "acc_prefetch", "acc_kb", "tile_fwd", "early_fwd", "pdl", "stage",
+   "jit_blocks_fwd" / "jit_blocks_rev". */
 int svg_engine_set_option(svg_engine* e, const char* key, int64_t value);
 
 /* The hot path: one full adjoint sweep.  sums_out[num_params] receives the
