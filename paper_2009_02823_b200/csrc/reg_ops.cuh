@@ -328,7 +328,7 @@ __device__ __forceinline__ void unstage(double2 (&v)[1 << R], const double2* stg
 // One register op with its structure as template arguments (jit.cpp): the same
 // steps as the interpreted kernel's op loop, with every mask a literal.
 template <int R, int NB, int V, uint32_t XL, uint32_t ZLW, uint32_t CLW, uint32_t SMASK, uint32_t CMASK,
-          uint64_t ZO, uint64_t CO, bool RBI, uint32_t SLOT, bool RET = false>
+          uint64_t ZO, uint64_t CO, bool RBI, uint32_t SLOT, bool RET = false, int PSIGN = -1>
 __device__ __forceinline__ double jit_op(double2 (&v)[1 << R], double2 (&l)[1 << R], uint64_t sbase, uint32_t tbase,
                                          double ca, double cbb, double kr, double2 ka, double2 kb, const IpSink& sink) {
   if (CO != 0 && (sbase & CO) != CO) return 0.0;
@@ -342,7 +342,9 @@ __device__ __forceinline__ double jit_op(double2 (&v)[1 << R], double2 (&l)[1 <<
   c.smask = SMASK;
   c.cmask = CMASK;
   c.clw_ok = (tbase & CLW) == CLW;
-  c.pneg = c.bb < 0.0;
+  // signed permutations (fixed Paulis): the sign is structural and, without
+  // lane / warp / off-tile Z factors, a literal (PSIGN 0 / 1) -- no sign flips
+  c.pneg = PSIGN >= 0 ? uint32_t(PSIGN) : uint32_t(c.bb < 0.0);
   return op_body<R, NB, V, RET>(v, l, c, XL, slw, RBI, SLOT, kr, ka, kb, sink);
 }
 
