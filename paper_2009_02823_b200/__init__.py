@@ -16,6 +16,7 @@ from .adjoint import (
     LiveStateAudit,
     OpCounters,
     circuit_expectation,
+    finite_difference_gradient,
     non_hermitian_gradient,
     reverse_mode_gradient,
     sweep,
@@ -45,5 +46,6 @@ from .ir import (
 )
 from .operators import BUILTIN_OBSERVABLES, Observable, adjoint_observable, builtin_observable
 from .state import BasisState, StateVector, clone_state, init_basis_state, inner_product
+from .textio import CircuitParseError, ObservableParseError, circuit_to_text, observable_to_text, parse_circuit, parse_observable
 
 __version__ = "0.1.0"

@@ -140,3 +140,38 @@ def circuit_expectation(circuit, params, obs, input_state, *, device: int = 0, e
     problem = Problem(circuit, params, obs, input_state)
     energy, _ = (engine or _native.engine(device)).expectation(problem.c)
     return complex(energy.re, energy.im)
+
+
+DEFAULT_FD_STEP = 1e-5  # svgrad/gradients.py DEFAULT_FD_STEP
+
+
+def finite_difference_gradient(circuit, params, obs, input_state, delta: float = DEFAULT_FD_STEP, *,
+                               device: int = 0, engine=None) -> GradientReport:
+    """Central differences on the GPU expectation path (svgrad/gradients.py:262-294).
+
+    2P + 1 forward sweeps (forward passes + observable kernel each); counters
+    follow the reference's per-evaluation accounting: G gate applications, one
+    clone and one observable application per expectation.
+    """
+    if delta <= 0:
+        raise ValueError(f"delta must be positive, got {delta}")
+    params = _check_call(circuit, params, obs, input_state)
+    counters = OpCounters()
+    G = len(circuit.gates)
+
+    def evaluate(theta):
+        counters.clones += 1
+        counters.gate_applies += G
+        counters.observable_applies += 1
+        return circuit_expectation(circuit, theta, obs, input_state, device=device, engine=engine)
+
+    values = np.zeros(circuit.num_params, dtype=complex)
+    shifted = params.copy()
+    for k in range(circuit.num_params):
+        shifted[k] = params[k] + delta
+        plus = evaluate(shifted)
+        shifted[k] = params[k] - delta
+        minus = evaluate(shifted)
+        shifted[k] = params[k]
+        values[k] = (plus - minus) / (2.0 * delta)
+    return GradientReport(values, evaluate(params), counters)
