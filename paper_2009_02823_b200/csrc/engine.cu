@@ -200,6 +200,7 @@ struct svg_engine {
   int64_t opt_scale_carry = 1;   // generated kernels: deferred scale carried across layout changes
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
   int64_t opt_early_fwd = 1;     // one shard: launch the forward passes while the rest is lowered
+  int64_t opt_direct_store = 0;  // free-lane passes store from a non-global lane layout (no final transpose)
   int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
@@ -946,7 +947,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         }
         L.segs.push_back(sd);
       }
-      if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
+      if (prev_l != ~0u && prev_l != 31u && !e->opt_direct_store) {  // back to the global lane layout for the store
         SegLocal sl;
         SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, kf, RF, &sl);
         sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
@@ -1171,7 +1172,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
           }
           L.segs.push_back(sd);
         }
-        if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
+        if (prev_l != ~0u && prev_l != 31u && !e->opt_direct_store) {  // back to the global lane layout for the store
           SegLocal sl;
           SegDesc sd = make_seg(SEG_REG, default_regs(RB), 31u, l.swz, L.k, RB, &sl);
           sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
@@ -1945,6 +1946,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "lane_cost10" || k == "xpose_cost10") {
     if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
     (k == "lane_cost10" ? e->opt_lane_cost10 : e->opt_xpose_cost10) = value;
+  } else if (k == "direct_store") {
+    e->opt_direct_store = value != 0;
   } else if (k == "early_fwd") {
     e->opt_early_fwd = value != 0;
   } else if (k == "tile_fwd") {
