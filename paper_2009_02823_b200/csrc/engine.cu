@@ -125,11 +125,6 @@ enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG, L_SWAP, L_
 // layout (lanes on positions 0..4) is conflict-free for every choice.
 struct Swizzle {
   uint8_t col[32] = {1, 2, 4};
-  bool identity() const {
-    for (int p = 3; p < 32; ++p)
-      if (col[p]) return false;
-    return true;
-  }
 };
 
 struct Launch {

@@ -345,7 +345,6 @@ std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, c
       }
       if (best <= best_count && popc(regs) > 0) {
         // no single position unlocks a gate: take the flip set of the earliest ready gate
-        std::vector<int> pred_ready;
         for (int i = 0; i < m; ++i)
           if (!done[i] && npred[i] == 0 && popc(regs | flip_pos[i]) <= regbits && (flip_pos[i] & ~regs)) {
             regs |= flip_pos[i];
