@@ -196,6 +196,7 @@ struct svg_engine {
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
   int64_t opt_early_fwd = 1;     // one shard: launch the forward passes while the rest is lowered
   int64_t opt_direct_store = 0;  // free-lane passes store from a non-global lane layout (no final transpose)
+  int64_t opt_early_stage = 0;   // reverse passes: stage the next tile's phi at tile start
   int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
@@ -1317,6 +1318,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.q = l->d.q;
       jp.swz = l->swz.col;
       jp.scale_carry = carry;
+      jp.early_stage = e->opt_early_stage != 0;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -1941,6 +1943,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "lane_cost10" || k == "xpose_cost10") {
     if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
     (k == "lane_cost10" ? e->opt_lane_cost10 : e->opt_xpose_cost10) = value;
+  } else if (k == "early_stage") {
+    e->opt_early_stage = value != 0;
   } else if (k == "direct_store") {
     e->opt_direct_store = value != 0;
   } else if (k == "early_fwd") {

@@ -33,6 +33,7 @@ struct JitPass {
   bool fuse_diag = true;             // reverse passes: fuse runs of diagonal rotations
   bool acc_prefetch = true;          // reverse passes: load an op's accumulator before the op
   bool scale_carry = false;          // deferred scale carried across layout changes (no shared-memory segments)
+  bool early_stage = false;          // reverse passes: next tile's phi staged at tile start (see jit.cu)
   bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
   int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;

@@ -61,6 +61,9 @@ _VARIANTS = {  # generated-kernel plan options (engine defaults: all on / auto)
     "direct_store": {"direct_store": 1},
     "direct_store_wide": {"direct_store": 1, "tile_qubits": 12},
     "no_early_fwd": {"early_fwd": 0},
+    "early_stage": {"early_stage": 1},
+    "early_stage_wide": {"early_stage": 1, "tile_qubits": 12},
+    "early_stage_fixed_lanes": {"early_stage": 1, "free_lanes": 0},
     "no_pdl_no_stage": {"pdl": 0, "stage": 0},
 }
 
@@ -81,7 +84,7 @@ def test_generated_kernel_variants_match_reference_golden(name, variant):
         rep = _run(circ, theta, obs, inp, method)
     finally:
         for k, v in {"jit": 1, "tile_qubits": 0, "tile_fwd": 0, "free_lanes": 1, "scale_carry": 1, "fuse_diag": 1,
-                     "acc_prefetch": 1, "acc_kb": 0, "lane_cost10": 37, "direct_store": 0, "early_fwd": 1,
+                     "acc_prefetch": 1, "acc_kb": 0, "lane_cost10": 37, "direct_store": 0, "early_fwd": 1, "early_stage": 0,
                      "pdl": 1, "stage": 1}.items():
             eng.set_option(k, v)
     assert max_err(rep.values, cvec(gold["values"])) <= GRAD_TOL
