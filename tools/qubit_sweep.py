@@ -27,6 +27,7 @@ def run(cfg, n):
         "ms_per_step": line["ms_per_step"], "phase_ms": line["phase_ms"], "passes": line["passes"],
         "rev_roofline_frac": line["roofline"]["frac"], "rev_achieved_gbs": line["roofline"]["achieved"],
         "effective_gate_level_gbs": line["effective_gate_level_gbs"], "state_bytes": S,
+        "rev_fp64_frac": (line.get("roofline_fp64") or {}).get("frac"),
         "clocks": line["clocks"],
     }
 
