@@ -336,3 +336,54 @@ def test_circuit_specialised_equals_interpreted(cfg, n):
     assert stats["jit_passes"] > 0
     assert max_err(rep.values, ref.values) <= 1e-11
     assert abs(rep.energy - ref.energy) <= ENERGY_TOL
+
+
+def _random_circuit(n, seed, num_gates=160):
+    """Seeded random mix of every register-capable gate shape (rotations on lane /
+    register / warp / off-tile qubits, controlled rotations, Pauli-product rotations,
+    fixed Paulis, CNOTs) plus a few dense gates, with repeated parameters."""
+    rng = np.random.default_rng([seed, n, 99])
+    gates, P = [], 24
+    for _ in range(num_gates):
+        r = rng.random()
+        q = [int(x) for x in rng.choice(n, size=3, replace=False)]
+        p = int(rng.integers(0, P))
+        if r < 0.30:
+            gates.append({0: sv.rx, 1: sv.ry, 2: sv.rz}[int(rng.integers(0, 3))](q[0], p))
+        elif r < 0.45:
+            gates.append({0: sv.crx, 1: sv.cry, 2: sv.crz}[int(rng.integers(0, 3))](q[0], q[1], p))
+        elif r < 0.60:
+            axes = "".join("XYZ"[int(i)] for i in rng.integers(0, 3, size=2))
+            gates.append(sv.rp(axes, (q[0], q[1]), p))
+        elif r < 0.72:
+            gates.append(sv.cx(q[0], q[1]))
+        elif r < 0.84:
+            gates.append(sv.fixed("xyz"[int(rng.integers(0, 3))], q[0]))
+        elif r < 0.90:
+            gates.append(sv.fixed("h", q[0]))
+        elif r < 0.95:
+            gates.append(sv.phase_gate(q[0], p))
+        else:
+            gates.append(sv.Gate(sv.PauliRotation("X", alpha=0.75), (q[0],), (q[1], q[2]), (p,)))
+    return sv.Circuit(n, tuple(gates), P)
+
+
+@pytest.mark.parametrize("n,seed", [(18, 1), (19, 2), (20, 3), (24, 4)])
+def test_random_circuits_match_oracle(n, seed):
+    """Randomised gate mixes at sizes where the generated kernels run with their
+    default plans (free-lane layouts, carried scales, fused diagonal runs, literal
+    permutation signs; 12-qubit tiles at 24 qubits) against the C oracle."""
+    from cases import mixed_observable
+    from oracle import oracle
+
+    circ = _random_circuit(n, seed, num_gates=120 if n >= 24 else 160)
+    theta = np.random.default_rng([seed, 5]).uniform(-np.pi, 2 * np.pi, circ.num_params)
+    obs = mixed_observable(sv, n, seed, count=10)
+    inp = sv.init_basis_state(n)
+    stats = {}
+    rep = sv.reverse_mode_gradient(circ, theta, obs, inp, stats=stats)
+    vals, energy, counters = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+    assert stats["jit_passes"] > 0
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
+    assert vars(rep.counters) == counters
