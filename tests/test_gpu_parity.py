@@ -387,3 +387,40 @@ def test_random_circuits_match_oracle(n, seed):
     assert max_err(rep.values, vals) <= GRAD_TOL
     assert abs(rep.energy - energy) <= ENERGY_TOL
     assert vars(rep.counters) == counters
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+def test_random_circuits_sharded_match_oracle(shards):
+    """The same random mixes split over virtual shards (qubit swaps, rank-bit signs
+    and controls, partner fetches) with the generated kernels (>= 18 local qubits)."""
+    from cases import mixed_observable, random_amplitudes
+    from oracle import oracle
+
+    n = 20
+    circ = _random_circuit(n, 10 + shards)
+    theta = np.random.default_rng([shards, 6]).uniform(-np.pi, 2 * np.pi, circ.num_params)
+    obs = mixed_observable(sv, n, shards, count=10)
+    inp = sv.StateVector(n, random_amplitudes(n, shards))
+    eng = sv.distributed.virtual_engine(shards)
+    eng.set_option("emulate_transport", 1)
+    stats = {}
+    rep = sv.reverse_mode_gradient(circ, theta, obs, inp, engine=eng, stats=stats)
+    vals, energy, _ = oracle.reverse_mode_values(circ, theta, obs, inp.amplitudes)
+    assert stats["jit_passes"] > 0 and stats["swaps"] > 0
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
+def test_random_circuit_non_hermitian_matches_oracle():
+    from cases import mixed_observable
+    from oracle import oracle
+
+    n = 19
+    circ = _random_circuit(n, 21)
+    theta = np.random.default_rng([21, 7]).uniform(-np.pi, 2 * np.pi, circ.num_params)
+    obs = mixed_observable(sv, n, 21, count=8, letters="XYZ+-", complex_coeffs=True)
+    inp = sv.init_basis_state(n, 5)
+    rep = sv.non_hermitian_gradient(circ, theta, obs, inp)
+    vals, energy, _ = oracle.non_hermitian_values(circ, theta, obs, inp.amplitudes)
+    assert max_err(rep.values, vals) <= GRAD_TOL
+    assert abs(rep.energy - energy) <= ENERGY_TOL
