@@ -225,11 +225,23 @@ __global__ void k_finalize(const double2* __restrict__ partials, const SumSpec* 
   const int lane = threadIdx.x & 31;
   if (i >= count) return;
   const SumSpec sp = specs[i];
-  double2 acc = make_double2(0.0, 0.0);
-  for (int64_t c = lane; c < sp.count; c += 32) {
-    const double2 v = partials[sp.off + c];
-    acc = make_double2(acc.x + v.x, acc.y + v.y);
+  // four independent accumulators (loads in flight together); the order of the
+  // additions is fixed by (lane, count), so reruns stay bit-identical
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+  const double2* p = partials + sp.off;
+  int64_t c = lane;
+  for (; c + 96 < sp.count; c += 128) {
+    const double2 v0 = p[c], v1 = p[c + 32], v2 = p[c + 64], v3 = p[c + 96];
+    a0 = make_double2(a0.x + v0.x, a0.y + v0.y);
+    a1 = make_double2(a1.x + v1.x, a1.y + v1.y);
+    a2 = make_double2(a2.x + v2.x, a2.y + v2.y);
+    a3 = make_double2(a3.x + v3.x, a3.y + v3.y);
   }
+  for (; c < sp.count; c += 32) {
+    const double2 v = p[c];
+    a0 = make_double2(a0.x + v.x, a0.y + v.y);
+  }
+  double2 acc = make_double2((a0.x + a1.x) + (a2.x + a3.x), (a0.y + a1.y) + (a2.y + a3.y));
   acc = warp_sum(acc);
   if (lane == 0) out[i] = acc;
 }
