@@ -86,3 +86,37 @@ def test_cli_fd_method(tmp_path, capsys):
     _, rev, _ = _parse_report(capsys.readouterr().out)
     for k in rev:
         assert abs(fd[k] - rev[k]) <= 1e-6
+
+
+def test_reverse_mode_time_is_linear_in_parameters():
+    """The paper's scaling claim as the reference's acceptance criterion 3 states it
+    for reverse mode (log-log slope of time vs P in [0.75, 1.35]; reference
+    pkg/tests/test_acceptance.py:97-117), here on the GPU at n = 20, P = 320..2560."""
+    import time
+
+    n = 20
+    obs = sv.Observable(n, tuple((1.0, "I" * i + "ZZ" + "I" * (n - i - 2)) for i in range(n - 1)))
+    inp = sv.BasisState(n)
+    ps, ts = [], []
+    for L in (8, 16, 32, 64):
+        gates, p = [], 0
+        for _ in range(L):
+            for q in range(n):
+                gates.append(sv.ry(q, p))
+                p += 1
+            for q in range(n):
+                gates.append(sv.rz(q, p))
+                p += 1
+            gates += [sv.cx(q, q + 1) for q in range(n - 1)]
+        circ = sv.Circuit(n, tuple(gates), p)
+        theta = np.random.default_rng([L]).uniform(0, 2 * np.pi, p)
+        sv.reverse_mode_gradient(circ, theta, obs, inp)  # compile / warm up
+        best = float("inf")
+        for _ in range(5):
+            t0 = time.perf_counter()
+            sv.reverse_mode_gradient(circ, theta, obs, inp)
+            best = min(best, time.perf_counter() - t0)
+        ps.append(p)
+        ts.append(best)
+    slope = np.polyfit(np.log(ps), np.log(ts), 1)[0]
+    assert 0.75 <= slope <= 1.35, (slope, ts)
