@@ -469,8 +469,9 @@ SegDesc make_seg(int kind, uint32_t regmask, uint32_t lanemask, const Swizzle& s
 constexpr double kMinDeferredA = 1e-3;
 constexpr double kMinDeferredC = 1e-60;
 // Auto mode compiles circuit-specialised kernels for shards of at least this
-// many qubits (smaller states: the one-off compile outweighs the pass time).
-constexpr int kJitMinQubits = 18;
+// many qubits (measured 1.8-2x the interpreter's gradients/s from 10 qubits on;
+// below 12 the first call's compile outweighs a few hundred microseconds of work).
+constexpr int kJitMinQubits = 12;
 // Gates per register-tile pass: beyond ~40 the straight-line pass kernels
 // outgrow the instruction cache (measured: cfg 3 reverse 115 ms at 96, 105 ms at 40).
 constexpr int kRegPassGates = 40;
@@ -681,6 +682,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // per SM; fewer passes -- measured cfg 3 reverse -7 %, cfg 4 -9 %)
   if (e->opt_tile == 0 && jit_expected && nloc >= kWideTileQubits && (int64_t(1) << (nloc - 12)) >= 2ll * e->sms)
     L.k = 12;
+  // small states (L2-resident, latency-bound passes): fewer, wider passes beat
+  // tile balance -- measured cfg 2 structure, n = 12 / 14 / 16 / 18: best k =
+  // 10 / 10 / 11 / 12 (2427 / 2134 / 1800 / 1490 gradients/s)
+  if (e->opt_tile == 0 && jit_expected && nloc <= 18 && nloc > 10) L.k = std::max(10, std::min(12, nloc - 5));
   L.b = (nloc <= L.k) ? nloc : std::min(5, L.k - 2);
   if (g > 0 && L.b < 5 && nloc > L.k) throw InvalidArg("sharded engines need >= 7 qubits per shard");
   // register bits (amplitudes per thread per buffer = 2^R): auto = 4 for the

@@ -392,7 +392,7 @@ def test_random_circuits_match_oracle(n, seed):
 @pytest.mark.parametrize("shards", [2, 4])
 def test_random_circuits_sharded_match_oracle(shards):
     """The same random mixes split over virtual shards (qubit swaps, rank-bit signs
-    and controls, partner fetches) with the generated kernels (>= 18 local qubits)."""
+    and controls, partner fetches) with the generated kernels (>= 12 local qubits)."""
     from cases import mixed_observable, random_amplitudes
     from oracle import oracle
 
