@@ -165,7 +165,7 @@ int svg_engine_set_stream(svg_engine* e, void* stream);
    "max_gates_per_pass" (0 = auto), "kernel" (0 auto, 1 shared-memory tiles, 2 register tiles),
    "reg_bits" / "reg_bits_fwd" (3 or 4: 2^bits amplitudes per thread in reverse / forward passes),
    "jit" (circuit-specialised register-tile kernels compiled at run time with NVRTC:
-   0 off, 1 auto = shards of >= 12 qubits, 2 always), "emulate_transport" (virtual engines:
+   0 off, 1 auto = shards of >= 10 qubits, 2 always), "emulate_transport" (virtual engines:
    run the NCCL data path with device copies), "prefetch" (ignored); generated-kernel plan
    options (defaults on / auto): "free_lanes", "lane_cost10", "xpose_cost10", "scale_carry",
    "fuse_diag", "acc_prefetch", "acc_kb", "tile_fwd", "early_fwd", "pdl", "stage",

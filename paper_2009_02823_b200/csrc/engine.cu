@@ -470,8 +470,8 @@ constexpr double kMinDeferredA = 1e-3;
 constexpr double kMinDeferredC = 1e-60;
 // Auto mode compiles circuit-specialised kernels for shards of at least this
 // many qubits (measured 1.8-2x the interpreter's gradients/s from 10 qubits on;
-// below 12 the first call's compile outweighs a few hundred microseconds of work).
-constexpr int kJitMinQubits = 12;
+// below 10 the first call's compile outweighs the few microseconds of work).
+constexpr int kJitMinQubits = 10;
 // Gates per register-tile pass: beyond ~40 the straight-line pass kernels
 // outgrow the instruction cache (measured: cfg 3 reverse 115 ms at 96, 105 ms at 40).
 constexpr int kRegPassGates = 40;
