@@ -98,33 +98,83 @@ def _traffic_per_launch(workload: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region.
+
+    In-process NVML polling every 5 ms (a timed region of a few tens of ms still
+    gets samples; the ctypes calls release the GIL), falling back to an
+    `nvidia-smi -lms` child process when NVML is unavailable.
+    """
 
     QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, interval_s: float = 0.005):
         self.device = device
+        self.interval = interval_s
         self.proc = None
+        self.nvml = None
+        self.samples: list[tuple[float, float, set]] = []  # (sm MHz, max MHz, reasons)
         self.lines: list[str] = []
+        self.stop = threading.Event()
 
     def __enter__(self):
         try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            idx = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(self.device)).split(",")[self.device]) \
+                if os.environ.get("CUDA_VISIBLE_DEVICES", "").replace(",", "").isdigit() else self.device
+            self.handle = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = nv
+            self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
         return self
 
+    def _sample(self):
+        nv = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        self.samples.append((float(sm), float(mx), {n for n, b in self.bits.items() if r & b}))
+
+    def _poll(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.stop.wait(self.interval)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.nvml is not None:
+            self.thread.join(timeout=1)
+            if not self.samples:  # at least one reading at the region's end
+                try:
+                    self._sample()
+                except Exception:
+                    pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -134,7 +184,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s_, m_, r_ in self.samples:
+            sm.append(s_)
+            mx = m_
+            reasons |= r_
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
@@ -144,12 +197,13 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for name, flag in zip(names, parts[3:7]):
+            for name, flag in zip(self.NAMES, parts[3:7]):
                 if flag.lower() == "active":
                     reasons.add(name)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def _cpu_port(w, inp, min_seconds=10.0, max_reps=5):
