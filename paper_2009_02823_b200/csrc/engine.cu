@@ -198,6 +198,7 @@ struct svg_engine {
   int64_t opt_direct_store = 0;  // free-lane passes store from a non-global lane layout (no final transpose)
   int64_t opt_early_stage = 0;   // reverse passes: stage the next tile's phi at tile start
   int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
+  int64_t opt_fwd_lane_cost10 = 50, opt_fwd_xpose_cost10 = 80;  // forward passes (one buffer)
   int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
   // reverse passes: shared-memory budget (KB) of the lane-group inner-product
   // accumulators; 0 = auto (interpreter 24 KB; generated kernels: whatever the
@@ -871,7 +872,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       if (!steps[si].swap) pass_segments(steps[si].pass, pgates[si], pshapes[si], L.k, RB, lc, xc, &psegs[si], &pswz[si]);
     for (size_t si = 0; si < fsteps.size(); ++si)
       if (!fsteps[si].swap)
-        pass_segments(fsteps[si].pass, fpgates[si], fpshapes[si], kf, RF, 5.0, 8.0, &psegs_f[si], &pswz_f[si]);
+        pass_segments(fsteps[si].pass, fpgates[si], fpshapes[si], kf, RF, 0.1 * double(e->opt_fwd_lane_cost10),
+                      0.1 * double(e->opt_fwd_xpose_cost10), &psegs_f[si], &pswz_f[si]);
   }
   auto reg_launch = [&](const Pass& ps, int nb, int kk) {
     Launch l;
@@ -1945,9 +1947,10 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "acc_kb") {
     if (value < 0 || value > 200) return fail(SVG_EINVAL, "acc_kb must be in [0 (auto), 200]");
     e->opt_acc_kb = value;
-  } else if (k == "lane_cost10" || k == "xpose_cost10") {
+  } else if (k == "lane_cost10" || k == "xpose_cost10" || k == "fwd_lane_cost10" || k == "fwd_xpose_cost10") {
     if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
-    (k == "lane_cost10" ? e->opt_lane_cost10 : e->opt_xpose_cost10) = value;
+    (k == "lane_cost10" ? e->opt_lane_cost10 : k == "xpose_cost10" ? e->opt_xpose_cost10
+                                            : k == "fwd_lane_cost10" ? e->opt_fwd_lane_cost10 : e->opt_fwd_xpose_cost10) = value;
   } else if (k == "early_stage") {
     e->opt_early_stage = value != 0;
   } else if (k == "direct_store") {
