@@ -115,3 +115,25 @@ def test_non_pauli_observable_letters_expand_exactly():
                           else "Z" if (s.z_mask >> q) & 1 else "I" for q in range(3))
         dense += s.coeff * pauli_product(letters)
     assert np.allclose(dense, dense_matrix(obs), atol=1e-15)
+
+
+@pytest.mark.parametrize("cfg,n,tile", [(2, 14, 0), (3, 20, 12), (5, 18, 0)])
+def test_generated_kernels_compile_for_sm100a(cfg, n, tile):
+    """Without a GPU: lower the config with circuit-specialised kernels forced on and
+    NVRTC-compile every distinct generated pass kernel for sm_100a (free-lane
+    layouts, swizzled transposes, tile-order staging, fused diagonal runs)."""
+    import ctypes as C
+
+    from paper_2009_02823_b200 import _native as N
+    from paper_2009_02823_b200.lowering import Problem
+
+    lib = N.load()
+    w = sv.build_workload(cfg, n)
+    pr = Problem(w.circuit, w.theta, w.observable, sv.BasisState(n), real_sums=True)
+    opts = (C.c_int64 * 4)(tile, 0, 0, 0)
+    count = C.c_int32()
+    rc = lib.svg_debug_jit_check(C.byref(pr.c), opts, C.byref(count))
+    if rc != 0 and b"NVRTC unavailable" in (lib.svg_last_error() or b""):
+        pytest.skip("libnvrtc not present")
+    assert rc == 0, lib.svg_last_error()
+    assert count.value > 0
