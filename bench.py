@@ -1,39 +1,46 @@
 #!/usr/bin/env python3
-"""Benchmark: full adjoint-gradient evaluations/s on a BASELINE.json config (default cfg 2).
+"""Benchmark: full adjoint-gradient evaluations/s on a BASELINE.json config (default cfg 4, n = 30).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
 One step = one full gradient (forward passes, observable, fused reverse
 passes, finalize) of the configured circuit.  Rank 0 prints ONE JSON line.
 
+Workload: BASELINE.json cfg 4 (n = 30, 16 GiB per state, G = 1424, P = 960,
+TFIM h = 0.7) -- the largest configuration that fits one GPU (cfg 5 needs
+3 x 128 GiB); ``--config`` selects another.  Synthetic: seeded generator
+(configs.py), |0..0> input; the state (2 x 16 GiB) is far larger than L2, and
+L2 is additionally flushed between timed steps.
+
 * ``value``: device-timed (CUDA events on the engine's stream = torch's
   current stream) throughput with the input state already in HBM (basis-state
   fast path); the per-call gate/term table upload (tens of KB) is inside.
-  L2 is flushed (256 MiB write) between timed steps, outside the events.
 * ``e2e``: the same metric through the public drop-in API with a HOST input
-  StateVector in pinned memory: Python lowering, H2D of the 2^n amplitudes and
-  tables, D2H of the P+1 results, all inside a wall-clock timed region.
-* ``roofline``: the dominant kernel (k_rev_pass, the fused reverse pass):
-  algorithmic bytes per launch = 4 * S (read+write phi and lambda, S = 16*2^n)
-  over its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs.
-* ``roofline_fp64``: the reverse sweep's algorithmic FP64 work (6 FMA per
-  amplitude per parametrised gate) over its device time, against the DFMA peak
-  measured on B200 (the reverse passes are FP64-bound above ~16 gates per pass,
-  profiles/README.md "pass cost model").
-* ``cpu_baseline``: the C restatement of the reference's schedule
-  (oracle/, "port") on the host cores, bounded sample (rank 0, N=1).
-* ``--impl reference``: that same CPU port as the reference arm.
+  state in pinned memory (a StateVector; on N > 1 each rank's ShardSlice):
+  Python lowering, H2D of the amplitudes and tables, D2H of the P+1 results,
+  all inside a wall-clock timed region.
+* ``roofline``: the dominant kernel (the fused reverse pass): algorithmic
+  bytes per launch = 4 * S (read+write phi and lambda, S = 16*2^n per shard)
+  over its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs;
+  ``traffic`` = ncu DRAM bytes of one such launch (profiles/ncu_rev_pass.json).
+* ``cpu_baseline`` (rank 0, N=1) and ``--impl reference``: the C restatement
+  of the reference's schedule (oracle/, "port") on all host cores.  A full
+  gradient of cfg 4 takes hours on the CPU (the reference itself needs
+  ~0.5 TiB), so a step is a bounded sample: every primitive the schedule calls
+  (1-qubit / controlled / 2-qubit apply_matrix, clone, inner product,
+  projection, observable axpy) timed once at the workload's full n, combined
+  with the schedule's exact primitive counts (oracle.op_counts) -- labelled
+  "extrapolated" with the counts and times in ``sample``; a calibration run
+  compares the model with a full oracle gradient at small n.
 
-Multi-GPU (torchrun, N>1), max-over-ranks device time:
-* configs BASELINE.json runs on one GPU (cfg 1-3; the default cfg 2 is
-  "Single GPU"): replicas -- each rank evaluates full gradients of its own
-  copy (no data-path collective), ``scaling: "weak"``, value = all ranks'
-  gradients / time;
-* the sharded configs (cfg 4 "strong-scaling ... sharded on its top qubits",
-  cfg 5) or ``--shard``: ONE state split over the N ranks by its top log2(N)
-  qubits (paper_2009_02823_b200.distributed.nccl_engine: NCCL half-shard
-  exchanges for qubit swaps, partner fetches, one all-gather of partial
-  sums), ``scaling: "strong"``, value = gradients of the whole job / time.
+Multi-GPU (N > 1; ``--gpus N`` self-launches N ranks with torch.distributed.run
+when WORLD_SIZE is unset, and must equal WORLD_SIZE when set), max-over-ranks
+device time:
+* cfg 4 / cfg 5 (default) or ``--shard``: ONE state split over the N ranks by
+  its top log2(N) qubits (NCCL half-shard exchanges for qubit swaps, partner
+  fetches, one all-gather of partial sums), ``scaling: "strong"``; at N = 8
+  the line also carries cfg 5 (n = 33, 128 GiB per state) under ``cfg5``;
+* cfg 1-3 ("Single GPU" in BASELINE.json): replicas, ``scaling: "weak"``.
 """
 from __future__ import annotations
 
@@ -61,7 +68,7 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--qubits", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tile-qubits", type=int, default=0)
@@ -77,6 +84,7 @@ def _args():
     ap.add_argument("--max-gates", type=int, default=0, help="gates per pass cap (0: planner default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="N=8: skip the extra cfg 5 measurement")
     return ap.parse_args()
 
 
@@ -206,53 +214,249 @@ class ClockSampler:
                 "source": "nvml" if self.samples else "nvidia-smi"}
 
 
-def _cpu_port(w, inp, min_seconds=10.0, max_reps=5):
+
+
+def _host_facts():
+    """CPU model, core counts and RAM of the host (BASELINE.md §3 asks for them beside the CPU number)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        mem = None
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "ram_bytes": mem}
+
+
+def _config_dict(w):
+    """The workload, identical in both arms (no implementation keys)."""
+    return {"workload": f"cfg{w.cfg}", "num_qubits": w.num_qubits, "num_gates": w.num_gates,
+            "num_params": w.circuit.num_params, "num_terms": len(w.observable.terms),
+            "state_bytes": 16 << w.num_qubits, "input": "|0..0>"}
+
+
+def _cpu_sample(w, threads):
+    """One bounded CPU sample of the oracle port: full gradients when the state is
+    small, else the primitive-time x exact-op-count model at the full n.
+    Returns (gradients/s, description dict)."""
     from oracle import oracle
 
-    threads = len(os.sched_getaffinity(0))
-    reps, t0 = 0, time.perf_counter()
-    while reps < max_reps:
-        oracle.reverse_mode_values(w.circuit, w.theta, w.observable, inp.amplitudes, threads=threads)
-        reps += 1
-        if time.perf_counter() - t0 >= min_seconds:
-            break
+    n = w.num_qubits
+    if n <= 22:  # a full gradient takes < ~10 s on 16 cores
+        t0 = time.perf_counter()
+        oracle.reverse_mode_values(w.circuit, w.theta, w.observable, _basis_amps(n),
+                                   threads=threads)
+        dt = time.perf_counter() - t0
+        return 1.0 / dt, {"mode": "full gradient", "seconds": dt}
+    counts = oracle.op_counts(w.circuit, w.observable)
+    t0 = time.perf_counter()
+    tp = oracle.time_primitives(n, threads)
     dt = time.perf_counter() - t0
-    return reps / dt, threads, reps, dt
+    T = sum(counts[k] * tp[k] for k in counts)
+    return 1.0 / T, {"mode": "extrapolated", "gradient_seconds": T, "sample_seconds": dt,
+                     "primitive_seconds": {k: round(v, 5) for k, v in tp.items()}, "op_counts": counts}
 
 
-def run_reference(args, rank):
-    """Reference arm: the C restatement of the reference's _reverse_sweep on all host cores."""
-    if rank != 0:
-        return
+_BASIS = {}
+
+
+def _basis_amps(n):
+    if n not in _BASIS:
+        import numpy as np
+
+        a = np.zeros(1 << n, dtype=np.complex128)
+        a[0] = 1.0
+        _BASIS[n] = a
+    return _BASIS[n]
+
+
+def _calibration(w, threads, n_cal=18):
+    """Model vs a full literal oracle gradient of the same structure at small n."""
     import paper_2009_02823_b200 as sv
     from oracle import oracle
 
+    wc = sv.build_workload(w.cfg, n_cal)
+    counts = oracle.op_counts(wc.circuit, wc.observable)
+    tp = oracle.time_primitives(n_cal, threads)
+    model = sum(counts[k] * tp[k] for k in counts)
+    t0 = time.perf_counter()
+    oracle.reverse_mode_values(wc.circuit, wc.theta, wc.observable, _basis_amps(n_cal), threads=threads)
+    meas = time.perf_counter() - t0
+    return {"n": n_cal, "measured_s": round(meas, 4), "model_s": round(model, 4), "ratio": round(meas / model, 3)}
+
+
+def _cpu_threads(n):
+    """All host threads, except for tiny states where OpenMP fork/join dominates (one thread)."""
+    return 1 if n <= 14 else len(os.sched_getaffinity(0))
+
+
+def _cpu_baseline(w):
+    threads = _cpu_threads(w.num_qubits)
+    val, desc = _cpu_sample(w, threads)
+    if desc["mode"] == "full gradient":
+        sample = f"1 full gradient of cfg{w.cfg} (n={w.num_qubits}) in {desc['seconds']:.2f} s"
+    else:
+        desc["calibration"] = _calibration(w, threads)
+        sample = (f"extrapolated: each primitive of oracle_sweep timed once at n={w.num_qubits} "
+                  f"({desc['sample_seconds']:.1f} s) x the exact primitive counts of one cfg{w.cfg} gradient "
+                  f"= {desc['gradient_seconds']:.0f} s per gradient (0 full gradients run at this size)")
+    return {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+            "detail": desc, "host": _host_facts()}
+
+
+def run_reference(args):
+    """Reference arm: the C restatement of the reference's _reverse_sweep (oracle/, "port") on all
+    host cores, each step one bounded sample of the workload (see _cpu_sample)."""
+    import paper_2009_02823_b200 as sv
+
     w = sv.build_workload(args.config, args.qubits)
-    inp = sv.init_basis_state(w.num_qubits)
-    threads = len(os.sched_getaffinity(0))
+    threads = _cpu_threads(w.num_qubits)
     for _ in range(args.warmup):
-        oracle.reverse_mode_values(w.circuit, w.theta, w.observable, inp.amplitudes, threads=threads)
+        _cpu_sample(w, threads)
+    vals, descs = [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.reverse_mode_values(w.circuit, w.theta, w.observable, inp.amplitudes, threads=threads)
+        v, d = _cpu_sample(w, threads)
+        vals.append(v)
+        descs.append(d)
     dt = time.perf_counter() - t0
-    value = args.steps / dt
-    sample = f"{args.steps} full gradients of cfg{args.config} (n={w.num_qubits}, G={w.num_gates})"
+    value = args.steps / sum(1.0 / v for v in vals)  # gradients / total (modelled) gradient time
+    d = descs[-1]
+    if d["mode"] == "full gradient":
+        sample = f"{args.steps} full gradients of cfg{args.config} (n={w.num_qubits}, G={w.num_gates})"
+    else:
+        d["calibration"] = _calibration(w, threads)
+        sample = (f"0 full gradients (one takes {1.0 / value:.0f} s here); per step every primitive of "
+                  f"oracle_sweep timed once at n={w.num_qubits} x the exact primitive counts of one gradient "
+                  f"(extrapolated; calibration at n={d['calibration']['n']}: measured/model "
+                  f"{d['calibration']['ratio']})")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (BASELINE cfg{args.config} generator, seed 0, |0..0> input)",
-        "config": {"workload": f"cfg{args.config}", "num_qubits": w.num_qubits, "num_gates": w.num_gates,
-                   "num_params": w.circuit.num_params, "num_terms": len(w.observable.terms)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "config": _config_dict(w),
+        "extrapolated": d["mode"] != "full gradient",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "detail": d, "host": _host_facts()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }))
 
 
-def run_ours(args, rank, world, local_rank):
+def _configure(eng, args):
+    eng.set_option("tile_qubits", args.tile_qubits)
+    if args.reg_bits:
+        eng.set_option("reg_bits", args.reg_bits)
+    if args.reg_bits_fwd:
+        eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
+    eng.set_option("stage", 0 if args.no_stage else 1)
+    eng.set_option("pdl", 0 if args.no_pdl else 1)
+    eng.set_option("fuse_diag", 0 if args.no_fuse_diag else 1)
+    eng.set_option("jit", args.jit)
+    eng.set_option("max_gates_per_pass", args.max_gates)
+    jb = [int(x) for x in args.jit_blocks.split(",")]
+    eng.set_option("jit_blocks_fwd", jb[0])
+    eng.set_option("jit_blocks_rev", jb[1])
+    for kv in args.opt:
+        key, val = kv.split("=")
+        eng.set_option(key, int(val))
+
+
+def _measure(args, w, eng, sharded, rank, world, local_rank, dist, steps, warmup, with_e2e):
+    """Warm-up, then `steps` timed gradients (CUDA events, L2 flushed between steps),
+    then the e2e leg through the public API with pinned host inputs."""
     import numpy as np
+    import torch
+
+    import paper_2009_02823_b200 as sv
+
+    n = w.num_qubits
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    basis = sv.BasisState(n)
+
+    def step(inp, st):
+        return sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp, stats=st, engine=eng)
+
+    for _ in range(warmup):
+        step(basis, {})
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    acc = {"rev_ms": 0.0, "rev_launches": 0, "launches": 0}
+    phases = {"forward": 0.0, "observable": 0.0, "reverse": 0.0, "other": 0.0}
+    last, st_last = None, None
+    with ClockSampler(local_rank) as clocks:
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            st = {}
+            ev[i][0].record(stream)
+            last = step(basis, st)
+            ev[i][1].record(stream)
+            acc["rev_ms"] += st["ms_reverse"]
+            for key in phases:
+                phases[key] += st[f"ms_{key}"] / steps
+            acc["rev_launches"] += st["rev_passes"]
+            acc["launches"] += st["launches"]
+            st_last = st
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        total_ms = float(t.item())
+    torch.cuda.synchronize()
+
+    e2e = None
+    if with_e2e:
+        # pinned host input: the whole state (one process) or this rank's slice (sharded)
+        local = (1 << n) // world if sharded else (1 << n)
+        pinned = torch.empty(local, dtype=torch.complex128, pin_memory=True)
+        host = pinned.numpy()
+        host[:] = 0
+        if not sharded or rank == 0:
+            host[0] = 1.0
+        state = sv.ShardSlice(n, host, rank, world) if sharded else sv.StateVector(n, host)
+        assert state.amplitudes.ctypes.data == host.ctypes.data  # no hidden pageable copy
+        st = {}
+        step(state, st)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        wall = 0.0
+        rep = None
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = step(state, st)
+            wall += time.perf_counter() - t0
+        e2e = {"value": steps / wall, "unit": UNIT,
+               "h2d_bytes_per_step": int(st["h2d_bytes"]), "d2h_bytes_per_step": int(st["d2h_bytes"])}
+        if dist:
+            t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["value"] = steps / float(t.item())
+        assert np.array_equal(rep.values, last.values)
+        del pinned, host, state
+    del flush
+    return {"total_ms": total_ms, "phases": phases, "acc": acc, "st": st_last, "clocks": clocks.summary(),
+            "e2e": e2e, "last": last}
+
+
+def run_ours(args, rank, world, local_rank):
     import torch
 
     import paper_2009_02823_b200 as sv
@@ -271,101 +475,41 @@ def run_ours(args, rank, world, local_rank):
     sharded = world > 1 and (args.shard or args.config in (4, 5))
     if sharded:
         eng = sv.distributed.nccl_engine(local_rank)
+        print(f"[bench] rank {rank}/{world}: NCCL communicator over {world} ranks (device {local_rank}); "
+              f"state sharded on its top {world.bit_length() - 1} qubits", file=sys.stderr, flush=True)
         jobs = 1  # the N ranks compute one gradient together
     else:
         eng = _native.engine(local_rank)
         jobs = world  # independent replicas
     S_rank = S // world if sharded else S
-    eng.set_option("tile_qubits", args.tile_qubits)
-    if args.reg_bits:
-        eng.set_option("reg_bits", args.reg_bits)
-    if args.reg_bits_fwd:
-        eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
-    eng.set_option("stage", 0 if args.no_stage else 1)
-    eng.set_option("pdl", 0 if args.no_pdl else 1)
-    eng.set_option("fuse_diag", 0 if args.no_fuse_diag else 1)
-    eng.set_option("jit", args.jit)
-    eng.set_option("max_gates_per_pass", args.max_gates)
-    jb = [int(x) for x in args.jit_blocks.split(",")]
-    eng.set_option("jit_blocks_fwd", jb[0])
-    eng.set_option("jit_blocks_rev", jb[1])
-    for kv in args.opt:
-        key, val = kv.split("=")
-        eng.set_option(key, int(val))
-    stream = torch.cuda.current_stream()
-    eng.set_stream(stream.cuda_stream)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    basis = sv.BasisState(n)
-
-    def step(inp, st):
-        return sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp, stats=st, engine=eng)
-
-    for _ in range(args.warmup):
-        step(basis, {})
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    rev_ms, rev_launches, launches, pass_bytes, last, tile_k = 0.0, 0, 0, 0, None, 0
-    phases = {"forward": 0.0, "observable": 0.0, "reverse": 0.0, "other": 0.0}
-    with ClockSampler(local_rank) as clocks:
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            st = {}
-            ev[i][0].record(stream)
-            last = step(basis, st)
-            ev[i][1].record(stream)
-            rev_ms += st["ms_reverse"]
-            for key in phases:
-                phases[key] += st[f"ms_{key}"] / args.steps
-            rev_launches += st["rev_passes"]
-            launches += st["launches"]
-            pass_bytes = st["pass_bytes"]
-            tile_k = st["tile_qubits"]
-            st_last = st
-        torch.cuda.synchronize()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-        total_ms = float(t.item())
-    torch.cuda.synchronize()
-
-    e2e = None
-    if not args.no_e2e and not (sharded and S > (4 << 30)):
-        # (sharded n >= 29: the API's full-size host StateVector on every rank would
-        # need N x S of pinned host memory; e2e is reported for the unsharded runs)
-        pinned = torch.empty(1 << n, dtype=torch.complex128, pin_memory=True)
-        host = pinned.numpy()
-        host[:] = 0
-        host[0] = 1.0
-        state = sv.StateVector(n, host)
-        assert state.amplitudes.ctypes.data == host.ctypes.data  # no hidden pageable copy
-        st = {}
-        step(state, st)
-        torch.cuda.synchronize()
-        wall = 0.0
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            rep = step(state, st)
-            wall += time.perf_counter() - t0
-        e2e = {"value": jobs * args.steps / wall, "unit": UNIT,
-               "h2d_bytes_per_step": int(st["h2d_bytes"]), "d2h_bytes_per_step": int(st["d2h_bytes"])}
-        if dist:
-            t = torch.tensor([wall], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e["value"] = jobs * args.steps / float(t.item())
-        assert np.array_equal(rep.values, last.values)
+    _configure(eng, args)
+    m = _measure(args, w, eng, sharded, rank, world, local_rank, dist, args.steps, args.warmup,
+                 with_e2e=not args.no_e2e)
+    st_last = m["st"]
+    extra = None
+    if sharded and world == 8 and args.config == 4 and args.qubits is None and not args.no_extra:
+        # BASELINE.json cfg 5 (n = 33) is the 8-GPU configuration: measured in the same job
+        eng.close()
+        torch.cuda.empty_cache()
+        w5 = sv.build_workload(5)
+        eng5 = sv.distributed.nccl_engine(local_rank)
+        _configure(eng5, args)
+        k5 = max(2, min(args.steps, 4))
+        m5 = _measure(args, w5, eng5, True, rank, world, local_rank, dist, k5, 1, with_e2e=not args.no_e2e)
+        s5 = m5["st"]
+        extra = {"config": _config_dict(w5), "value": k5 / (m5["total_ms"] * 1e-3), "unit": UNIT,
+                 "steps": k5, "warmup": 1, "ms_per_step": m5["total_ms"] / k5, "scaling": "strong",
+                 "parallelism": f"state sharded over {world} ranks (top 3 qubits)",
+                 "swaps_per_gradient": int(s5["swaps"]), "exchange_bytes_per_rank": int(s5["exchange_bytes"]),
+                 "phase_ms": {k: round(v, 3) for k, v in m5["phases"].items()}, "e2e": m5["e2e"],
+                 "clocks": m5["clocks"]}
+        eng5.close()
 
     if rank != 0:
         return
     peak, peak_src = _peak()
-    avg_launch_ms = rev_ms / max(1, rev_launches)
+    acc, phases, total_ms = m["acc"], m["phases"], m["total_ms"]
+    avg_launch_ms = acc["rev_ms"] / max(1, acc["rev_launches"])
     achieved = 4 * S_rank / (avg_launch_ms * 1e-3) / 1e9
     traffic = _traffic_per_launch(f"cfg{args.config}") if args.qubits is None and world == 1 else None
     value = jobs * args.steps / (total_ms * 1e-3)
@@ -373,32 +517,33 @@ def run_ours(args, rank, world, local_rank):
     n_param_gates = sum(1 for g in w.circuit.gates if len(g.param_refs) > 0)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cval, cores, reps, secs = _cpu_port(w, sv.init_basis_state(n))
-        cpu = {"value": cval, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{reps} full gradient(s) of cfg{args.config} in {secs:.1f} s (oracle/svgrad_oracle.c, OpenMP)"}
+        cpu = _cpu_baseline(w)
+    e2e = m["e2e"]
+    if e2e is not None:
+        e2e["value"] *= jobs
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (BASELINE cfg{args.config} generator, seed 0, |0..0> input; random-init theta)",
-        "config": {
-            "workload": f"cfg{args.config}", "num_qubits": n, "num_gates": w.num_gates,
-            "num_params": w.circuit.num_params, "num_terms": len(w.observable.terms),
-            "state_bytes": S, "l2": "flushed between timed steps (256 MiB write, outside the events)",
+        "config": _config_dict(w),
+        "run": {
             "parallelism": (f"state sharded over {world} ranks (top {world.bit_length() - 1} qubits)" if sharded
-                            else "replicas" if world > 1 else "single-gpu"), "tile_qubits": tile_k,
-            "swaps_per_gradient": int(st_last["swaps"]), "exchange_bytes_per_rank": int(st_last["exchange_bytes"]),
+                            else "replicas" if world > 1 else "single-gpu"),
+            "l2": "state (2 x S) >> L2; L2 also flushed between timed steps (256 MiB write, outside the events)",
+            "tile_qubits": int(st_last["tile_qubits"]), "swaps_per_gradient": int(st_last["swaps"]),
+            "exchange_bytes_per_rank": int(st_last["exchange_bytes"]),
+            "nccl_ranks": world if sharded else 0,
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "reverse register-tile pass (generated svgb_jit; interpreter k_pass_reg<4,2>)",
+            "traffic": traffic, "kernel": "fused reverse register-tile pass (generated svgb_jit)",
             "bytes_per_launch": 4 * S_rank,
             "avg_launch_ms": avg_launch_ms, "peak_source": peak_src,
         },
-        # the reverse sweep is FP64-bound above ~16 gates per pass: its algorithmic
-        # FP64 work is 6 FMA (12 flop) per amplitude per parametrised gate (rewind
-        # phi and lambda: 2 FMA each, Re<lambda|K|phi>: 2), against the DFMA peak
-        # measured with tools/ubench/peaks.cu (profiles/r01_ubench_peaks.jsonl)
+        # the reverse sweep's algorithmic FP64 work: 6 FMA (12 flop) per amplitude per
+        # parametrised gate (rewind phi and lambda: 2 FMA each, Re<lambda|K|phi>: 2),
+        # against the DFMA peak measured with tools/ubench/peaks.cu
         "roofline_fp64": {
             "kernel": "reverse sweep (all reverse passes)", "unit": "TFLOP/s",
             "flop_per_gradient": 12 * (S_rank // 16) * n_param_gates,
@@ -411,22 +556,57 @@ def run_ours(args, rank, world, local_rank):
         "passes": {"forward": int(st_last["fwd_passes"]), "observable": int(st_last["obs_passes"]),
                    "reverse": int(st_last["rev_passes"])},
         "effective_gate_level_gbs": B_alg / (total_ms / args.steps * 1e-3) / 1e9,
-        "pass_level_gbs": pass_bytes / (total_ms / args.steps * 1e-3) / 1e9,
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+        "pass_level_gbs": st_last["pass_bytes"] / (total_ms / args.steps * 1e-3) / 1e9,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": acc["launches"], "clocks": m["clocks"],
     }
-    print(json.dumps(line))
+    if extra is not None:
+        line["cfg5"] = extra
+    print(json.dumps(line), flush=True)
+
+
+def _self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: launch N ranks on this node."""
+    import socket
+
+    try:
+        import torch
+
+        have = torch.cuda.device_count()
+    except Exception:
+        have = 0
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     args = _args()
+    world_env = os.environ.get("WORLD_SIZE")
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
-        run_reference(args, rank)
-    else:
-        run_ours(args, rank, world, local_rank)
+        if rank == 0:  # the CPU arm runs once (rank 0); other ranks exit without work
+            run_reference(args)
+        return 0
+    if world_env is None and args.gpus > 1:
+        return _self_launch(args)
+    world = int(world_env or 1)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if world > 1:
+        # NCCL's communicator init lines (rank count) on stderr; stdout carries the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    run_ours(args, rank, world, int(os.environ.get("LOCAL_RANK", 0)))
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -105,6 +105,9 @@ typedef struct {
 
 /* svg_problem.flags */
 #define SVG_FLAG_REAL_SUMS 1  /* only Re(sums) is needed (Hermitian 2*Re path); imag may be 0 */
+#define SVG_FLAG_INPUT_LOCAL 2 /* input_amps holds only this engine's amplitudes: on an NCCL rank the
+                                  2^(n - log2 world) amplitudes of its shard (indices rank * 2^(n - log2
+                                  world) ...), elsewhere the whole state; no per-rank 2^n host array */
 
 typedef struct {
   int32_t num_qubits;

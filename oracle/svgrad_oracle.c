@@ -229,6 +229,200 @@ int oracle_sweep(const oracle_problem* p, cplx* sums, cplx* energy, oracle_count
   return 0;
 }
 
+/* ---------------------------------------------------------------------------
+ * Large-n variant of oracle_sweep (n = 30 fixtures on a host with tens of GiB):
+ * the same schedule, counters and per-amplitude arithmetic, with two storage
+ * economies that do not change any value the reference computes:
+ *   - input given as a basis index (init_basis_state, svgrad/statevector.py:43-53)
+ *     instead of a 2^n host array;
+ *   - the derivative probe (clone + derivative action + projection + inner
+ *     product, svgrad/gradients.py:161-165 with svgrad/circuit.py:302-334) is
+ *     evaluated group by group instead of being materialised: for each group of
+ *     the gate's targets the probe amplitudes are formed exactly as the
+ *     materialised sequence forms them (sigma per axis as a 2x2 product, then the
+ *     bound matrix, then the control projection) and contracted with the bra at
+ *     once.  Only the order of the inner product's floating-point sum differs.
+ *   - the observable is applied to ket (a clone of bra holding the same values),
+ *     so the pre-observable bra is released first: peak 3 states, 2 in the sweep.
+ * Checked against oracle_sweep on every golden case (tests/test_oracle.py).
+ * ------------------------------------------------------------------------- */
+static cplx deriv_inner(const oracle_problem* p, int d, const cplx* bra, const cplx* ket, int n, int nt,
+                        const int32_t* tg, int nc, const int32_t* cg) {
+  int64_t cmask = 0;
+  for (int k = 0; k < nc; ++k) cmask |= (int64_t)1 << cg[k];
+  int fixed[64];
+  int nf = 0;
+  for (int k = 0; k < nt; ++k) fixed[nf++] = tg[k];
+  qsort(fixed, nf, sizeof(int), cmp_int);
+  int64_t off[4] = {0, 0, 0, 0};
+  for (int k = 0; k < nt; ++k) {
+    const int64_t half = (int64_t)1 << k;
+    for (int64_t s = 0; s < half; ++s) off[half + s] = off[s] + ((int64_t)1 << tg[k]);
+  }
+  const int g = 1 << nt;
+  const int64_t groups = (int64_t)1 << (n - nf);
+  const int kind = p->dkind[d];
+  const cplx* dm = p->dmat + 16 * d;
+  double re = 0, im = 0;
+#pragma omp parallel for schedule(static) reduction(+ : re, im)
+  for (int64_t gi = 0; gi < groups; ++gi) {
+    int64_t idx = gi;
+    for (int f = 0; f < nf; ++f) {
+      const int64_t low = idx & (((int64_t)1 << fixed[f]) - 1);
+      idx = ((idx >> fixed[f]) << (fixed[f] + 1)) | low;
+    }
+    cplx v[4], w[4];
+    for (int s = 0; s < g; ++s) v[s] = ket[idx + off[s]];
+    if (kind == DK_PAULI_ROTATION) {
+      for (int k = 0; k < nt; ++k) {  /* sigma on target k: 1-target apply_matrix */
+        const cplx* m = PAULI[p->daxes[2 * d + k]];
+        const int b = 1 << k;
+        for (int s = 0; s < g; ++s) {
+          if (s & b) continue;
+          const cplx v0 = v[s], v1 = v[s | b];
+          v[s] = m[0] * v0 + m[1] * v1;
+          v[s | b] = m[2] * v0 + m[3] * v1;
+        }
+      }
+    }
+    if (kind == DK_PHASE) {  /* project_to_one on the targets */
+      for (int s = 0; s < g; ++s) w[s] = (s == g - 1) ? v[s] : 0;
+    } else if (g == 2) {  /* the bound rotation / dM, as apply_matrix does it */
+      w[0] = dm[0] * v[0] + dm[1] * v[1];
+      w[1] = dm[2] * v[0] + dm[3] * v[1];
+    } else {
+      for (int r = 0; r < g; ++r) {
+        cplx acc = 0;
+        for (int s = 0; s < g; ++s) acc += dm[r * g + s] * v[s];
+        w[r] = acc;
+      }
+    }
+    if ((idx & cmask) != cmask) continue;  /* control projection: the probe is 0 here */
+    for (int s = 0; s < g; ++s) {
+      const cplx z = conj(bra[idx + off[s]]) * w[s];
+      re += creal(z);
+      im += cimag(z);
+    }
+  }
+  return re + I * im;
+}
+
+int oracle_sweep_lean(const oracle_problem* p, int64_t basis, cplx* sums, cplx* energy, oracle_counters* cnt) {
+#ifdef _OPENMP
+  if (p->num_threads > 0) omp_set_num_threads(p->num_threads);
+#endif
+  const int n = p->num_qubits;
+  const int64_t dim = (int64_t)1 << n;
+  const size_t bytes = sizeof(cplx) * (size_t)dim;
+  cplx* ket = malloc(bytes);
+  if (!ket) return 1;
+  memset(cnt, 0, sizeof(*cnt));
+  for (int q = 0; q < p->num_params; ++q) sums[q] = 0;
+  if (p->input) {
+    copy_state(ket, p->input, n);
+  } else {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < dim; ++i) ket[i] = 0;
+    ket[basis] = 1;
+  }
+  cnt->clones++;  /* bra = clone_state(input) */
+  for (int i = 0; i < p->num_gates; ++i) {
+    apply_matrix(ket, n, p->fwd + 16 * i, p->ntargets[i], p->targets + 2 * i,
+                 p->ctrl_off[i + 1] - p->ctrl_off[i], p->controls + p->ctrl_off[i]);
+    cnt->gate_applies++;
+  }
+  cnt->clones++;  /* ket = clone_state(bra): same values, kept in `ket` */
+  cplx* bra = malloc(bytes);
+  cplx* scratch = malloc(bytes);
+  if (!bra || !scratch) {
+    free(ket); free(bra); free(scratch);
+    return 1;
+  }
+  apply_observable(p, ket, bra, scratch);  /* bra = apply_observable(bra, obs) */
+  cnt->observable_applies++;
+  free(scratch);
+  *energy = inner(ket, bra, n);
+
+  int d_end = p->num_derivs;
+  for (int i = p->num_gates - 1; i >= 0; --i) {
+    const int nt = p->ntargets[i];
+    const int32_t* tg = p->targets + 2 * i;
+    const int nc = p->ctrl_off[i + 1] - p->ctrl_off[i];
+    const int32_t* cg = p->controls + p->ctrl_off[i];
+    const int d0 = d_end - p->arity[i];
+    apply_matrix(ket, n, p->rewind + 16 * i, nt, tg, nc, cg);
+    cnt->gate_applies++;
+    for (int d = d0; d < d_end; ++d) {
+      cnt->clones++;
+      cnt->derivative_applies++;
+      sums[p->dref[d]] += p->dscalar[d] * deriv_inner(p, d, bra, ket, n, nt, tg, nc, cg);
+      cnt->inner_products++;
+    }
+    d_end = d0;
+    if (i > 0) {
+      apply_matrix(bra, n, p->adjoint + 16 * i, nt, tg, nc, cg);
+      cnt->gate_applies++;
+    }
+  }
+  free(bra); free(ket);
+  return 0;
+}
+
+/* Per-primitive wall times (seconds) on 2^n states, for the op-count model of
+ * oracle_sweep's cost (bench.py's CPU baseline): out[0] 1-target apply_matrix,
+ * [1] 1-target with one control, [2] 2-target apply_matrix, [3] clone,
+ * [4] inner product, [5] project_to_one (1 qubit), [6] observable axpy,
+ * [7] observable zero fill. */
+int oracle_time_primitives(int n, int threads, double* out) {
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#endif
+  const int64_t dim = (int64_t)1 << n;
+  const size_t bytes = sizeof(cplx) * (size_t)dim;
+  cplx* a = malloc(bytes);
+  cplx* b = malloc(bytes);
+  if (!a || !b) {
+    free(a); free(b);
+    return 1;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < dim; ++i) {
+    a[i] = (double)(i & 1023) * 1e-3 + I * 1e-3;
+    b[i] = 0;
+  }
+  const double c = 0.8, s = 0.6;
+  const cplx m1[4] = {c, -s, s, c};
+  const cplx m2[16] = {c - I * s, 0, 0, 0, 0, c + I * s, 0, 0, 0, 0, c + I * s, 0, 0, 0, 0, c - I * s};
+  const int32_t t1[1] = {n / 2}, t2[2] = {n / 2, n / 2 + 1}, ctl[1] = {n / 2 - 1};
+  volatile double sink = 0;
+  for (int k = 0; k < 8; ++k) {
+    const double t0 = omp_get_wtime();
+    switch (k) {
+      case 0: apply_matrix(a, n, m1, 1, t1, 0, NULL); break;
+      case 1: apply_matrix(a, n, m1, 1, t1, 1, ctl); break;
+      case 2: apply_matrix(a, n, m2, 2, t2, 0, NULL); break;
+      case 3: copy_state(b, a, n); break;
+      case 4: sink += creal(inner(a, b, n)); break;
+      case 5: project_to_one(b, n, 1, t1); break;
+      case 6: {
+        const cplx cc = 0.5;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < dim; ++i) b[i] += cc * a[i];
+        break;
+      }
+      case 7: {
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < dim; ++i) b[i] = 0;
+        break;
+      }
+    }
+    out[k] = omp_get_wtime() - t0;
+  }
+  (void)sink;
+  free(a); free(b);
+  return 0;
+}
+
 /* <psi|H|psi> after the forward pass only (svgrad/observable.py:114-116). */
 int oracle_expectation(const oracle_problem* p, cplx* energy) {
 #ifdef _OPENMP

@@ -45,7 +45,7 @@ from .ir import (
     rz,
 )
 from .operators import BUILTIN_OBSERVABLES, Observable, adjoint_observable, builtin_observable
-from .state import BasisState, StateVector, clone_state, init_basis_state, inner_product
+from .state import BasisState, ShardSlice, StateVector, clone_state, init_basis_state, inner_product
 from .textio import CircuitParseError, ObservableParseError, circuit_to_text, observable_to_text, parse_circuit, parse_observable
 
 __version__ = "0.1.0"

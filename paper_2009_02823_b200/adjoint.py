@@ -22,6 +22,7 @@ import numpy as np
 from . import _native
 from .lowering import Problem
 from .operators import adjoint_observable, is_hermitian
+from .state import ShardSlice
 
 
 @dataclass
@@ -90,6 +91,15 @@ def _account(counters, audit, num_gates: int, num_derivs: int) -> None:
     audit.release()
 
 
+def _check_slice(input_state, eng) -> None:
+    """A ShardSlice input must be the slice of the rank this engine is."""
+    if isinstance(input_state, ShardSlice):
+        rank = eng.rank if eng.rank is not None else 0
+        if eng.shards != input_state.world or rank != input_state.rank or (eng.shards > 1 and eng.rank is None):
+            raise ValueError(f"input slice is rank {input_state.rank} of {input_state.world}; "
+                             f"the engine is rank {eng.rank} of {eng.shards} shards")
+
+
 def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, stats: dict | None = None,
           real_sums: bool = False, engine=None):
     """Equivalent of the reference's ``_reverse_sweep``: (complex sums[P], energy).
@@ -97,8 +107,9 @@ def sweep(circuit, params, obs, input_state, counters, audit, device: int = 0, s
     ``real_sums=True`` lets the engine skip Im(sums) (returned as 0) when the
     caller only forms 2*Re, as the Hermitian path does (svgrad/gradients.py:198).
     """
-    problem = Problem(circuit, params, obs, input_state, real_sums=real_sums)
     eng = engine or _native.engine(device)
+    _check_slice(input_state, eng)
+    problem = Problem(circuit, params, obs, input_state, real_sums=real_sums)
     sums, _, energy, st = eng.reverse_sweep(problem.c, circuit.num_params, problem.num_derivs)
     _account(counters, audit, len(circuit.gates), problem.num_derivs)
     out = sums
@@ -137,8 +148,10 @@ def non_hermitian_gradient(circuit, params, obs, input_state, *, device: int = 0
 def circuit_expectation(circuit, params, obs, input_state, *, device: int = 0, engine=None) -> complex:
     """<psi(theta)|H|psi(theta)> via the forward passes and the observable kernel only."""
     params = _check_call(circuit, params, obs, input_state)
+    eng = engine or _native.engine(device)
+    _check_slice(input_state, eng)
     problem = Problem(circuit, params, obs, input_state)
-    energy, _ = (engine or _native.engine(device)).expectation(problem.c)
+    energy, _ = eng.expectation(problem.c)
     return complex(energy.re, energy.im)
 
 
@@ -159,10 +172,11 @@ def finite_difference_gradient(circuit, params, obs, input_state, delta: float =
     counters = OpCounters()
     G = len(circuit.gates)
 
-    def evaluate(theta):
+    def evaluate(theta):  # the reference's expectation(): clone, G applies, observable, one inner product
         counters.clones += 1
         counters.gate_applies += G
         counters.observable_applies += 1
+        counters.inner_products += 1
         return circuit_expectation(circuit, theta, obs, input_state, device=device, engine=engine)
 
     values = np.zeros(circuit.num_params, dtype=complex)

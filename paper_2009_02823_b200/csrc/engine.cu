@@ -1448,7 +1448,9 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     bool input_copied = false;
     if (p->input_amps) {
       const size_t amps0 = (size_t(1) << (p->num_qubits - e->shard_bits)) * e->shards_local;
-      const size_t first0 = e->comm ? size_t(e->rank) * (size_t(1) << (p->num_qubits - e->shard_bits)) : 0;
+      // SVG_FLAG_INPUT_LOCAL: the host array is this rank's slice only (no 2^n host copy per rank)
+      const size_t first0 = (e->comm && !(p->flags & SVG_FLAG_INPUT_LOCAL))
+                                ? size_t(e->rank) * (size_t(1) << (p->num_qubits - e->shard_bits)) : 0;
       e->psi.reserve(amps0 * sizeof(double2));
       CK(cudaMemcpyAsync(e->psi.ptr, p->input_amps + first0, amps0 * sizeof(double2), cudaMemcpyHostToDevice,
                          e->stream));
@@ -1626,8 +1628,9 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     // input: shards are consecutive slices of the full index range (identity layout at the start)
     const size_t first_amp = e->comm ? size_t(e->rank) * shard_amps : 0;
     if (p->input_amps) {
+      const size_t src_off = (p->flags & SVG_FLAG_INPUT_LOCAL) ? 0 : first_amp;
       if (!input_copied)
-        CK(cudaMemcpyAsync(psi, p->input_amps + first_amp, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(psi, p->input_amps + src_off, amps * sizeof(double2), cudaMemcpyHostToDevice, s));
       h2d += amps * sizeof(double2);
     } else if (!init_done) {
       CK(cudaMemsetAsync(psi, 0, amps * sizeof(double2), s));

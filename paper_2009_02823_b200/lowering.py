@@ -53,6 +53,7 @@ TERM_DTYPE = np.dtype(
 )
 _PAULI_FIXED = {"X": SIGMA["X"], "Y": SIGMA["Y"], "Z": SIGMA["Z"]}
 FLAG_REAL_SUMS = 1  # SVG_FLAG_REAL_SUMS: only 2*Re(sums) is consumed (Hermitian observables)
+FLAG_INPUT_LOCAL = 2  # SVG_FLAG_INPUT_LOCAL: input_amps is this rank's shard slice (state.ShardSlice)
 
 
 @dataclass
@@ -241,8 +242,11 @@ class Problem:
         self.num_derivs = len(self.derivs)
         from .state import basis_index_of
 
+        from .state import ShardSlice
+
         basis = basis_index_of(input_state)
         self.amps = None
+        local = isinstance(input_state, ShardSlice)
         if basis is None:
             self.amps = np.ascontiguousarray(input_state.amplitudes, dtype=np.complex128)
         p = N.svg_problem()
@@ -251,7 +255,7 @@ class Problem:
         p.num_gates = len(self.gates)
         p.num_derivs = self.num_derivs
         p.num_terms = len(self.terms)
-        p.flags = FLAG_REAL_SUMS if real_sums else 0
+        p.flags = (FLAG_REAL_SUMS if real_sums else 0) | (FLAG_INPUT_LOCAL if local else 0)
         p.gates = self.gates.ctypes.data_as(C.POINTER(N.svg_gate))
         p.derivs = self.derivs.ctypes.data_as(C.POINTER(N.svg_deriv))
         p.terms = self.terms.ctypes.data_as(C.POINTER(N.svg_pauli_term))

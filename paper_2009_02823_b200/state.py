@@ -73,6 +73,36 @@ class BasisState:
         return f"BasisState(num_qubits={self.num_qubits}, basis_index={self.basis_index})"
 
 
+class ShardSlice:
+    """This rank's slice of a ``num_qubits`` input state for a sharded NCCL engine.
+
+    A rank of a job sharded over ``world`` GPUs by the top log2(world) qubits
+    holds amplitudes ``rank * 2^m .. (rank + 1) * 2^m - 1`` (m = n - log2(world)).
+    Passing this slice instead of the full StateVector keeps the host side of each
+    rank at 16 * 2^m bytes (the reference's StateVector would be the whole 2^n
+    array on every rank: 128 GiB at n = 33).  Same ``num_qubits`` semantics as
+    StateVector; ``amplitudes`` is the local slice.
+    """
+
+    __slots__ = ("num_qubits", "amplitudes", "rank", "world")
+
+    def __init__(self, num_qubits: int, amplitudes, rank: int, world: int):
+        _check_size(num_qubits)
+        if world < 1 or world & (world - 1) or not 0 <= rank < world or world > (1 << num_qubits):
+            raise ValueError(f"bad rank {rank} / world {world} for {num_qubits} qubits")
+        amps = np.asarray(amplitudes, dtype=np.complex128)
+        local = (1 << num_qubits) // world
+        if amps.shape != (local,):
+            raise ValueError(f"expected {local} local amplitudes, got shape {amps.shape}")
+        self.num_qubits = num_qubits
+        self.amplitudes = amps
+        self.rank = rank
+        self.world = world
+
+    def __repr__(self) -> str:
+        return f"ShardSlice(num_qubits={self.num_qubits}, rank={self.rank}, world={self.world})"
+
+
 def init_basis_state(num_qubits: int, basis_index: int = 0) -> StateVector:
     """|basis_index> as a dense StateVector (reference ``svgrad/statevector.py:43-53``)."""
     basis = BasisState(num_qubits, basis_index)

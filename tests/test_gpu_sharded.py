@@ -188,3 +188,42 @@ def test_nccl_engine_single_rank(name):
     rep = _run(circ, theta, obs, inp, method, eng)
     assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg5_n15", "cfg3_n14"])
+def test_nccl_engine_single_rank_slice_input(name):
+    """A dense host input handed to an NCCL rank as its ShardSlice (SVG_FLAG_INPUT_LOCAL):
+    one rank of one -> the slice is the whole state; same result as the StateVector."""
+    from paper_2009_02823_b200 import _native
+
+    rec = GOLD[name]
+    circ, theta, obs, inp, method = materialize(SMALL[name])
+    eng = _native.Engine(0, shards=1, rank=0, nccl_id=_native.nccl_unique_id())
+    dense = sv.StateVector(circ.num_qubits, inp.amplitudes)
+    sl = sv.ShardSlice(circ.num_qubits, np.array(inp.amplitudes), 0, 1)
+    a = sv.reverse_mode_gradient(circ, theta, obs, dense, engine=eng)
+    b = sv.reverse_mode_gradient(circ, theta, obs, sl, engine=eng)
+    assert np.array_equal(a.values, b.values) and a.energy == b.energy
+    assert max_err(b.values, cvec(rec["values"])) <= GRAD_TOL
+    with pytest.raises(ValueError, match="slice"):
+        sv.reverse_mode_gradient(circ, theta, obs, sv.ShardSlice(circ.num_qubits, np.array(
+            inp.amplitudes[: len(inp.amplitudes) // 2]), 1, 2), engine=eng)
+
+
+@pytest.mark.slow
+def test_cfg5_structure_n30_eight_virtual_shards_vs_oracle_fixture():
+    """cfg 5's structure (RX/RY/RZ + RZZ chain, 128 random Pauli strings) at n = 30 over
+    8 virtual shards with the NCCL data path emulated (half-shard pack/exchange/unpack,
+    partner fetches), against the full-size oracle fixture (tests/golden/make_oracle_n30.py):
+    every entry <= 1e-10 abs-or-rel, energy <= 1e-12."""
+    gold = load_golden("oracle_cfg5_n30.json")["cfg5_n30"]
+    w = sv.build_workload(5, 30)
+    eng = sv.distributed.virtual_engine(8)
+    eng.set_option("emulate_transport", 1)
+    stats = {}
+    rep = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, sv.BasisState(30), engine=eng, stats=stats)
+    eng.close()
+    assert stats["swaps"] >= 1
+    assert max_err(rep.values, np.asarray(gold["values_real"], dtype=complex)) <= GRAD_TOL
+    assert abs(rep.energy - complex(*gold["energy"])) <= ENERGY_TOL
+    assert vars(rep.counters) == gold["counters"]

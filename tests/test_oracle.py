@@ -54,3 +54,75 @@ def test_oracle_thread_count_invariance():
     one = oracle.sweep(circ, theta, obs, inp.amplitudes, threads=1)
     many = oracle.sweep(circ, theta, obs, inp.amplitudes, threads=4)
     assert max_err(many.sums, one.sums) <= 1e-12
+
+
+@pytest.mark.parametrize("name", sorted(n for n in CASES if GOLD[n]["method"] == "reverse"))
+def test_lean_sweep_matches_reference_golden(name):
+    """oracle_sweep_lean (the n = 30 fixture generator: probe contracted group by
+    group, basis-index input) against the reference's own outputs."""
+    rec = GOLD[name]
+    circ, theta, obs, inp, _ = materialize(CASES[name])
+    r = oracle.sweep_lean(circ, theta, obs, inp.amplitudes)
+    assert max_err(2.0 * r.sums.real, cvec(rec["values"])) <= 1e-12
+    assert abs(r.energy - complex(*rec["energy"])) <= 1e-12
+    assert r.counters == rec["counters"]
+
+
+@pytest.mark.parametrize("cfg,n", [(4, 16), (5, 15), (3, 14), (2, 14)])
+def test_lean_sweep_matches_literal_with_basis_input(cfg, n):
+    import paper_2009_02823_b200 as sv
+
+    w = sv.build_workload(cfg, n)
+    a = oracle.sweep(w.circuit, w.theta, w.observable, sv.init_basis_state(n).amplitudes)
+    b = oracle.sweep_lean(w.circuit, w.theta, w.observable, None, 0)
+    assert max_err(b.sums, a.sums) <= 1e-13
+    assert abs(a.energy - b.energy) <= 1e-13
+    assert a.counters == b.counters
+
+
+def test_op_count_model_matches_counters():
+    """oracle.op_counts (bench.py's CPU-baseline model) counts the same schedule the
+    counters report: gate applies = 3G-1 plus the derivative/observable applies."""
+    import paper_2009_02823_b200 as sv
+
+    w = sv.build_workload(4, 8)
+    c = oracle.op_counts(w.circuit, w.observable)
+    G, A = w.num_gates, w.circuit.num_params
+    factors = sum(sum(ch != "I" for ch in f) for _, f in w.observable.terms)
+    assert c["apply_1q"] + c["apply_1q_ctrl"] + c["apply_2q"] == (3 * G - 1) + 2 * A + factors
+    assert c["clone"] == A + 2 + len(w.observable.terms)
+    assert c["inner"] == A + 1
+
+
+def test_n30_fixtures_are_pinned_to_this_oracle():
+    """The committed n = 30 fixtures (tests/golden/make_oracle_n30.py) match the
+    workload generator and the oracle source they were produced from."""
+    import hashlib
+    import json
+    import os
+
+    import paper_2009_02823_b200 as sv
+    from golden.make_golden import circuit_digest, obs_digest
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    found = 0
+    for name, (cfg, n) in {"cfg4": (4, None), "cfg5_n30": (5, 30)}.items():
+        path = os.path.join(here, f"oracle_{name}.json")
+        if not os.path.exists(path):
+            continue
+        found += 1
+        rec = json.load(open(path))["cases"][name]
+        w = sv.build_workload(cfg, n)
+        assert rec["circuit_digest"] == circuit_digest(w.circuit)
+        assert rec["obs_digest"] == obs_digest(w.observable)
+        assert rec["theta_sum"] == pytest.approx(float(np.sum(w.theta)), abs=0)
+        assert len(rec["values_real"]) == w.circuit.num_params
+        G, A = w.num_gates, w.circuit.num_params
+        assert rec["counters"] == {"gate_applies": 3 * G - 1, "derivative_applies": A, "clones": A + 2,
+                                   "inner_products": A, "observable_applies": 1}
+        assert rec["sums_imag_max"] >= 0.0
+        with open(oracle.SRC, "rb") as f:
+            src = hashlib.sha256(f.read()).hexdigest()
+        assert rec["oracle_sha256"] == src, "oracle source changed since the fixture was generated"
+    if not found:
+        pytest.skip("no n = 30 fixtures generated yet")
