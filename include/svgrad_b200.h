@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SVG_ABI_VERSION 1
+#define SVG_ABI_VERSION 2
 #define SVG_MAX_QUBITS 40
 
 typedef struct { double re, im; } svg_c128;
@@ -93,7 +93,8 @@ typedef struct {
   svg_c128 k[16];
 } svg_deriv;
 
-/* One Pauli string of the observable (letters H,+,- pre-expanded on the host).
+/* One Pauli string of the observable (terms with few H,+,- letters pre-expanded
+ * on the host; wider ones go to svg_product_term).
  * Replaces the per-term loop of apply_observable (svgrad/observable.py:79-100). */
 typedef struct {
   svg_c128 coeff;
@@ -102,6 +103,24 @@ typedef struct {
   int32_t n_y;
   int32_t reserved;
 } svg_pauli_term;
+
+/* One product term coeff * (x)_q F_q of the observable with arbitrary 2x2
+ * factors F_q (row-major, on distinct qubits): the letters H, + and - (and any
+ * Pauli letters of the same term) as matrices, applied factor by factor --
+ * Walsh-Hadamard butterflies for H -- instead of an expansion into 2^w Pauli
+ * strings (hadamard_all = 2^N strings; svgrad/observable.py:19-27,79-100,
+ * svgrad/bench.py:94).  factors[first_factor .. first_factor + num_factors). */
+typedef struct {
+  svg_c128 coeff;
+  int32_t first_factor;
+  int32_t num_factors;
+} svg_product_term;
+
+typedef struct {
+  int32_t qubit;
+  int32_t reserved;
+  svg_c128 m[4];
+} svg_factor;
 
 /* svg_problem.flags */
 #define SVG_FLAG_REAL_SUMS 1  /* only Re(sums) is needed (Hermitian 2*Re path); imag may be 0 */
@@ -121,6 +140,11 @@ typedef struct {
   const svg_pauli_term* terms;
   int64_t input_basis;       /* |input_basis> when input_amps == NULL */
   const svg_c128* input_amps;/* host array of 2^n amplitudes, or NULL */
+  /* ABI 2: product terms (applied after the Pauli strings; the observable is the sum of both) */
+  int32_t num_product_terms;
+  int32_t num_factors;
+  const svg_product_term* product_terms;
+  const svg_factor* factors;
 } svg_problem;
 
 typedef struct {

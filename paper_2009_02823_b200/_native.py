@@ -11,7 +11,7 @@ import os
 import threading
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvgb200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 SVG_OK, SVG_EINVAL, SVG_ENOMEM, SVG_ECUDA, SVG_ENCCL, SVG_EUNSUPPORTED = range(6)
 FORM_PAULI, FORM_MAT = 0, 1
@@ -58,6 +58,14 @@ class svg_pauli_term(C.Structure):
     ]
 
 
+class svg_product_term(C.Structure):
+    _fields_ = [("coeff", c128), ("first_factor", C.c_int32), ("num_factors", C.c_int32)]
+
+
+class svg_factor(C.Structure):
+    _fields_ = [("qubit", C.c_int32), ("reserved", C.c_int32), ("m", c128 * 4)]
+
+
 class svg_problem(C.Structure):
     _fields_ = [
         ("num_qubits", C.c_int32), ("num_params", C.c_int32), ("num_gates", C.c_int32),
@@ -65,6 +73,8 @@ class svg_problem(C.Structure):
         ("gates", C.POINTER(svg_gate)), ("derivs", C.POINTER(svg_deriv)),
         ("terms", C.POINTER(svg_pauli_term)), ("input_basis", C.c_int64),
         ("input_amps", C.c_void_p),
+        ("num_product_terms", C.c_int32), ("num_factors", C.c_int32),
+        ("product_terms", C.POINTER(svg_product_term)), ("factors", C.POINTER(svg_factor)),
     ]
 
 

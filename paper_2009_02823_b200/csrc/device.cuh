@@ -141,6 +141,18 @@ struct SegDesc {
 };
 static_assert(sizeof(SegDesc) == 48, "SegDesc layout");
 
+// One pass of a product term's pipeline (k_prod_pass): the 2x2 factors whose
+// qubits sit in this pass's tile, applied one after the other as butterflies
+// over the shared-memory tile (Walsh-Hadamard for H).  Not last: the tile goes
+// to the product buffer; last: lambda (+)= scalar * tile and the energy partial.
+constexpr int kMaxProdFactors = 16;
+struct ProdFactors {
+  int32_t n;     // factors in this pass
+  int32_t last;  // 1: accumulate into lambda (d.accumulate) with the energy partial
+  uint32_t pos[kMaxProdFactors];            // tile-local positions
+  double2 m[kMaxProdFactors][4];            // row-major 2x2 matrices
+};
+
 // Entry of the finalize map: deterministic sum of `count` partials at `off`.
 struct SumSpec {
   int64_t off;

@@ -53,6 +53,13 @@ struct CudaError : std::runtime_error {
   CudaError(cudaError_t c, const char* what)
       : std::runtime_error(std::string(what) + ": " + cudaGetErrorString(c)), code(c) {}
 };
+// Generating / compiling / loading a circuit-specialised kernel failed (NVRTC
+// missing or too old for sm_100a, load error): auto mode re-lowers for the
+// interpreted kernels; forced mode (jit = 2) reports SVG_ECUDA.
+struct JitFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 struct InvalidArg : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -115,7 +122,7 @@ struct HostBuf {
   }
 };
 
-enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG, L_SWAP, L_FETCH };
+enum LaunchKind { L_SMEM_FWD, L_SMEM_REV, L_OBS, L_OBS_DIRECT, L_REG, L_SWAP, L_FETCH, L_PROD };
 
 // Shared-memory swizzle of a pass's transposes: element e of a tile lives at
 // e ^ sum_{p >= 3, bit p of e set} col[p] (3-bit columns, bits 0..2).  A warp's
@@ -139,6 +146,13 @@ struct Launch {
   int gbit = 0, lpos = 0;  // L_SWAP: rank bit <-> local position
   std::shared_ptr<JitKernel> jit;  // L_REG: circuit-specialised kernel (jit.cu), or null: interpreter
   Swizzle swz;                     // L_REG: shared-memory swizzle of the pass's transposes
+  // L_PROD: this pass's factors; first pass reads psi (or the partner shard), later
+  // ones the product buffer; the last one's scalar per source shard is
+  // coeff * sum_j w_j (-1)^popcount(src rank bits & zg_j) (rank-bit factors in Pauli form)
+  ProdFactors prod = {};
+  bool prod_first = false;
+  double2 prod_coeff = {0.0, 0.0};
+  std::vector<std::pair<uint64_t, double2>> prod_z;
 };
 
 // Everything a sweep needs on the host side, built from one svg_problem.
@@ -194,6 +208,7 @@ struct svg_engine {
   int64_t opt_free_lanes = 1;    // generated kernels: free-lane segment plans where cheaper
   int64_t opt_scale_carry = 1;   // generated kernels: deferred scale carried across layout changes
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
+  int64_t opt_low_qubits = 3;    // generated kernels: contiguous low qubits every tile holds (3..5)
   int64_t opt_early_fwd = 1;     // one shard: launch the forward passes while the rest is lowered
   int64_t opt_direct_store = 0;  // free-lane passes store from a non-global lane layout (no final transpose)
   int64_t opt_early_stage = 0;   // reverse passes: stage the next tile's phi at tile start
@@ -213,7 +228,7 @@ struct svg_engine {
   mutable std::unordered_map<Key128, std::vector<Segment>, Key128Hash> seg_memo;
   mutable std::unordered_map<Key128, std::pair<std::shared_ptr<const std::vector<Segment>>, Swizzle>, Key128Hash> choice_memo;
   mutable std::unordered_map<Key128, std::shared_ptr<const std::pair<std::vector<Step>, std::vector<int>>>, Key128Hash> plan_memo;  // why auto mode fell back to the interpreted kernels
-  DeviceBuf psi, lam, partials, blob, results, scratch, gathered;
+  DeviceBuf psi, lam, partials, blob, results, scratch, gathered, prodbuf;
   HostBuf hblob, hres;
   // sharding: the state is split over 2^shard_bits shards by its top physical
   // qubits; this engine holds `shards_local` of them (virtual shards on one
@@ -232,9 +247,11 @@ void validate(const svg_problem* p) {
   if (!p) throw InvalidArg("null problem");
   const int n = p->num_qubits;
   if (n < 1 || n > SVG_MAX_QUBITS) throw InvalidArg("num_qubits out of range");
-  if (p->num_gates < 0 || p->num_derivs < 0 || p->num_terms < 1 || p->num_params < 0)
+  if (p->num_gates < 0 || p->num_derivs < 0 || p->num_terms < 0 || p->num_params < 0 || p->num_product_terms < 0 ||
+      p->num_factors < 0 || p->num_terms + p->num_product_terms < 1)
     throw InvalidArg("negative table size or empty observable");
-  if ((p->num_gates && !p->gates) || (p->num_derivs && !p->derivs) || !p->terms)
+  if ((p->num_gates && !p->gates) || (p->num_derivs && !p->derivs) || (p->num_terms && !p->terms) ||
+      (p->num_product_terms && !p->product_terms) || (p->num_factors && !p->factors))
     throw InvalidArg("null table pointer");
   const uint64_t full = (n == 64) ? ~0ull : ((1ull << n) - 1);
   int d = 0;
@@ -266,6 +283,18 @@ void validate(const svg_problem* p) {
   for (int t = 0; t < p->num_terms; ++t) {
     const svg_pauli_term& tm = p->terms[t];
     if ((tm.x_mask | tm.z_mask) & ~full) throw InvalidArg("observable term outside register");
+  }
+  for (int t = 0; t < p->num_product_terms; ++t) {
+    const svg_product_term& pt = p->product_terms[t];
+    if (pt.first_factor < 0 || pt.num_factors < 0 || pt.first_factor + pt.num_factors > p->num_factors)
+      throw InvalidArg("product term " + std::to_string(t) + ": factor range outside the factor table");
+    uint64_t seen = 0;
+    for (int f = pt.first_factor; f < pt.first_factor + pt.num_factors; ++f) {
+      const int q = p->factors[f].qubit;
+      if (q < 0 || q >= n || ((seen >> q) & 1))
+        throw InvalidArg("product term " + std::to_string(t) + ": factor qubit out of range or repeated");
+      seen |= 1ull << q;
+    }
   }
   if (!p->input_amps && (p->input_basis < 0 || static_cast<uint64_t>(p->input_basis) > full))
     throw InvalidArg("basis index out of range");
@@ -665,7 +694,7 @@ thread_local std::chrono::steady_clock::time_point g_phase_t;
 // -- generated kernels only, no shared-memory segments -- so the caller can start
 // them while the rest (observable, reverse sweep) is still being lowered.
 Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
-              const std::function<void(Lowered&)>& fwd_ready = {}) {
+              const std::function<void(Lowered&)>& fwd_ready = {}, bool interp_only = false) {
   g_phase_t = std::chrono::steady_clock::now();
   Lowered L;
   const int n = p->num_qubits;
@@ -704,6 +733,15 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   };
   L.reg = e->opt_kernel != 1 && L.b >= 5 && fits(RB) && fits(RF);
   if (e->opt_kernel == 2 && !L.reg) throw InvalidArg("register-tile kernels need 5 + reg_bits .. 13 tile qubits");
+  // free-lane plans and carried scales need the generated kernels (the
+  // interpreter keeps lanes on tile positions 0..4)
+  const bool jit_planned = L.reg && !interp_only && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) &&
+                           (e->jit_dry_run || jit_available(nullptr));
+  L.jit_planned = jit_planned;
+  // Generated kernels address the global tile through the lanes' physical qubits, so
+  // their tiles need only qubits 0..low_qubits-1 (128-byte rows at 3) instead of
+  // 0..4: more tile qubits free for the circuit (cfg 4: 61 -> 52 passes per sweep)
+  if (jit_planned && nloc > L.k && e->opt_low_qubits < L.b) L.b = static_cast<int>(e->opt_low_qubits);
   PlanParams pp;
   pp.n = nloc;
   pp.k = L.k;
@@ -743,11 +781,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   };
   const auto sched = schedule(pp, &l2p_final);
   const std::vector<Step>& steps = sched->first;
-  // free-lane plans and carried scales need the generated kernels (the
-  // interpreter keeps lanes on tile positions 0..4)
-  const bool jit_planned = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits)) &&
-                           (e->jit_dry_run || jit_available(nullptr));
-  L.jit_planned = jit_planned;
   // The forward sweep only has to deliver psi at its end, so (one shard, generated
   // kernels) it runs its own schedule over larger tiles -- one buffer per tile
   // leaves room for 2^(k+1) amplitudes per CTA: fewer HBM passes.
@@ -998,7 +1031,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.op_begin = l.d.op_begin;
         passes.push_back(jp);
       }
-      std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->device);
+      std::vector<std::shared_ptr<JitKernel>> ks;
+      try {
+        ks = jit_get(passes, e->device);
+      } catch (const std::exception& ex) {
+        throw JitFailure(ex.what());
+      }
       for (size_t i = 0; i < ks.size(); ++i) {
         Launch& l = L.fwd[i];
         l.jit = ks[i];
@@ -1098,6 +1136,101 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       L.obs_kernels++;
       L.obs.push_back(l);
       L.pass_bytes += (l.d.accumulate ? 3 : 2) * S;
+    }
+  }
+
+  // Product terms (factors kept as 2x2 matrices, e.g. hadamard_all): per term a
+  // pipeline of tile passes, each applying the factors on its tile qubits; the
+  // last pass accumulates coeff * (x)F psi into lambda with the energy partial.
+  // Factors on rank bits (sharded states) are written in the Pauli basis
+  // (F = aI + bX + cY + dZ): every rank flip pattern is a sub-pipeline reading
+  // the partner shard, and the Z parts fold into a per-shard scalar.
+  for (int t = 0; t < p->num_product_terms; ++t) {
+    const svg_product_term& pt = p->product_terms[t];
+    std::vector<std::pair<int, const svg_c128*>> locf;
+    // rank-bit part: (x pattern, z pattern, weight), expanded factor by factor
+    std::vector<std::tuple<uint64_t, uint64_t, double2>> subs = {{0ull, 0ull, make_double2(1.0, 0.0)}};
+    for (int f = pt.first_factor; f < pt.first_factor + pt.num_factors; ++f) {
+      const int q = l2p_final.empty() ? p->factors[f].qubit : l2p_final[p->factors[f].qubit];
+      const svg_c128* m = p->factors[f].m;
+      if (q < nloc) {
+        locf.push_back({q, m});
+        continue;
+      }
+      const uint64_t bit = 1ull << q;
+      const double2 m0 = d2(m[0]), m1 = d2(m[1]), m2 = d2(m[2]), m3 = d2(m[3]);
+      // F = a I + b X + c Y + d Z; c Y with Y = i^1 (-1)^{((m^x)&z)} X-flip: weight c*i
+      const double2 a = make_double2(0.5 * (m0.x + m3.x), 0.5 * (m0.y + m3.y));
+      const double2 dz = make_double2(0.5 * (m0.x - m3.x), 0.5 * (m0.y - m3.y));
+      const double2 bx = make_double2(0.5 * (m1.x + m2.x), 0.5 * (m1.y + m2.y));
+      const double2 cy = make_double2(-0.5 * (m1.y - m2.y), 0.5 * (m1.x - m2.x));  // i (m01 - m10) / 2
+      const std::tuple<uint64_t, uint64_t, double2> parts[4] = {
+          {0ull, 0ull, a}, {bit, 0ull, bx}, {bit, bit, cm(cy, make_double2(0.0, 1.0))}, {0ull, bit, dz}};
+      std::vector<std::tuple<uint64_t, uint64_t, double2>> next;
+      for (const auto& sb : subs)
+        for (const auto& pa : parts) {
+          const double2 w = cm(std::get<2>(sb), std::get<2>(pa));
+          if (w.x == 0.0 && w.y == 0.0) continue;
+          next.push_back({std::get<0>(sb) | std::get<0>(pa), std::get<1>(sb) | std::get<1>(pa), w});
+        }
+      subs.swap(next);
+    }
+    std::sort(locf.begin(), locf.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    // tile passes over the local factor qubits: the forced low qubits plus up to
+    // kobs - b further factor qubits each (filled up with the lowest free qubits)
+    const uint64_t low = (L.b >= 64) ? ~0ull : ((1ull << L.b) - 1);
+    std::vector<std::vector<std::pair<int, const svg_c128*>>> chunks(1);
+    int wide = 0;
+    for (const auto& fq : locf) {
+      if ((low >> fq.first) & 1) {
+        chunks[0].push_back(fq);
+        continue;
+      }
+      if (wide == kobs - L.b || int(chunks.back().size()) >= kMaxProdFactors) {
+        chunks.emplace_back();
+        wide = 0;
+      }
+      chunks.back().push_back(fq);
+      ++wide;
+    }
+    // low-qubit factors ride in the first pass (chunk 0 may also hold wide ones)
+    std::map<uint64_t, std::vector<std::pair<uint64_t, double2>>> by_x;
+    for (const auto& sb : subs) by_x[std::get<0>(sb)].push_back({std::get<1>(sb), std::get<2>(sb)});
+    for (const auto& xz : by_x) {
+      const uint64_t xg = xz.first;
+      if (xg) {
+        L.obs.push_back(Launch{});
+        L.obs.back().kind = L_FETCH;
+        L.obs.back().d.xglob = xg;
+        L.swap_bytes += 2 * S;
+      }
+      for (size_t c = 0; c < chunks.size(); ++c) {
+        uint64_t qm = low;
+        for (const auto& fq : chunks[c]) qm |= 1ull << fq.first;
+        for (int q = 0; q < nloc && __builtin_popcountll(qm) < std::min(kobs, nloc); ++q) qm |= 1ull << q;
+        Launch l;
+        l.kind = L_PROD;
+        l.d = make_desc(nloc, __builtin_popcountll(qm), qm);
+        l.d.xglob = xg;
+        const TileMap tm = tile_map(qm);
+        l.prod.n = static_cast<int32_t>(chunks[c].size());
+        for (size_t j = 0; j < chunks[c].size(); ++j) {
+          l.prod.pos[j] = static_cast<uint32_t>(tm.pos[chunks[c][j].first]);
+          for (int r = 0; r < 4; ++r) l.prod.m[j][r] = d2(chunks[c][j].second[r]);
+        }
+        l.prod_first = c == 0;
+        l.prod.last = c + 1 == chunks.size();
+        if (l.prod.last) {
+          l.prod_coeff = d2(pt.coeff);
+          l.prod_z = xz.second;
+          l.d.accumulate = L.obs_kernels > 0;
+          L.obs_kernels++;
+          L.pass_bytes += (l.d.accumulate ? 4 : 3) * S;
+        } else {
+          L.pass_bytes += 2 * S;
+        }
+        L.obs.push_back(l);
+      }
     }
   }
 
@@ -1271,6 +1404,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         l.smem = obs_smem(l.d.k, l.d.b, l.d.op_end - l.d.op_begin);
         l.grid = clamp_grid_k(memo_occ(-3, 0, 0, l.smem, [&] { return occupancy(1, l.smem); }), ntiles_of(l));
         break;
+      case L_PROD:
+        l.smem = prod_smem(l.d.k, l.d.b);
+        l.grid = clamp_grid_k(memo_occ(-4, l.d.k, 0, l.smem, [&] { return occupancy(3, l.smem); }), ntiles_of(l));
+        break;
       case L_OBS_DIRECT:
         l.smem = 0;
         l.grid = std::max(1, static_cast<int>(std::min<int64_t>(int64_t(e->sms) * 8, int64_t(1) << std::max(0, nloc - 8))));
@@ -1364,7 +1501,9 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       }
     } catch (const std::exception& ex) {
       if (e->jit_dry_run && std::string(ex.what()) != "dry run") throw;
-      if ((e->opt_jit == 2 || L.free_lanes_used || carry) && !e->jit_dry_run) throw;
+      // plans made for the generated kernels (free lanes, carried scales, short
+      // tile rows) cannot run on the interpreter: the caller re-lowers
+      if ((e->opt_jit == 2 || L.free_lanes_used || carry || L.b < 5) && !e->jit_dry_run) throw JitFailure(ex.what());
       e->jit_error = ex.what();  // auto: keep the interpreted kernels
     }
   }
@@ -1441,6 +1580,8 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
   try {
     const auto t_enter = std::chrono::steady_clock::now();
     validate(p);
+    if (e->shard_bits > 0 && e->shards_local == 1 && !e->comm)
+      throw NcclError("the engine's NCCL communicator was aborted after an earlier failure");
     CK(cudaSetDevice(e->device));
     // A host input state starts its (large) host -> device copy before the host-side
     // lowering, which then overlaps the transfer; shards are consecutive slices of
@@ -1495,7 +1636,19 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         CK(cudaEventRecord(e->ev[2], e->stream));
       };
     }
-    const Lowered L = lower(e, p, with_reverse, fwd_cb);
+    bool init_done = early;  // psi initialised before the lowering (ev[0], ev[1] recorded)
+    Lowered L;
+    try {
+      L = lower(e, p, with_reverse, fwd_cb);
+    } catch (const JitFailure& ex) {
+      if (e->opt_jit == 2) throw;
+      // auto mode: generated kernels unavailable -- plan again for the interpreted
+      // kernels; psi is set up again (early forward launches may have run)
+      e->jit_error = ex.what();
+      L = lower(e, p, with_reverse, {}, true);
+      init_done = false;
+      input_copied = false;
+    }
     const auto t_lowered = std::chrono::steady_clock::now();
     const int nloc = L.nloc;
     const int nsh = e->shards_local;       // shards held by this engine
@@ -1515,6 +1668,9 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     e->hres.reserve(cnt * std::max(nsh, world) * sizeof(double2));
     const bool emulate = !e->comm && nsh > 1 && e->opt_emulate_transport;
     if (emulate) e->scratch.reserve(2 * shard_amps * sizeof(double2));
+    bool multi_pass_products = false;  // a product pipeline of >= 2 passes keeps its tile in prodbuf
+    for (const Launch& l : L.obs) multi_pass_products = multi_pass_products || (l.kind == L_PROD && !l.prod.last);
+    if (multi_pass_products) e->prodbuf.reserve(amps * sizeof(double2));
     if (e->comm) {
       e->scratch.reserve(shard_amps * sizeof(double2));
       e->gathered.reserve(cnt * world * sizeof(double2));
@@ -1620,7 +1776,6 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     };
     int64_t launches = 0, h2d = bl.total, d2h = 0;
     const auto t_launch = std::chrono::steady_clock::now();
-    const bool init_done = early;  // psi initialised before the lowering (ev[0], ev[1] recorded)
     if (!init_done) CK(cudaEventRecord(e->ev[0], s));
     CK(cudaMemcpyAsync(db, hb, bl.total, cudaMemcpyHostToDevice, s));
     if (!e->blob_ev) CK(cudaEventCreateWithFlags(&e->blob_ev, cudaEventDisableTiming));
@@ -1660,6 +1815,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       }
     }
     if (!L.fwd_early) CK(cudaEventRecord(e->ev[2], s));
+    double2* prodbuf = static_cast<double2*>(e->prodbuf.ptr);
     for (const Launch& l : L.obs) {
       if (l.kind == L_FETCH) {
         if (e->comm) fetch_partner(l.d.xglob);
@@ -1670,10 +1826,27 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         PassDesc d = l.d;
         d.rank_bits = v.rank_bits;
         const double2* src = v.psi;
-        if (l.d.xglob) src = e->comm ? scratch : psi + ((uint64_t(sh) ^ (l.d.xglob >> nloc)) << nloc);
-        if (l.d.xglob && emulate) {  // partner shard -> scratch, as fetch_partner does over NCCL
+        const bool reads_partner = l.d.xglob && (l.kind != L_PROD || l.prod_first);
+        if (reads_partner) src = e->comm ? scratch : psi + ((uint64_t(sh) ^ (l.d.xglob >> nloc)) << nloc);
+        if (reads_partner && emulate) {  // partner shard -> scratch, as fetch_partner does over NCCL
           CK(cudaMemcpyAsync(scratch, src, shard_amps * sizeof(double2), cudaMemcpyDeviceToDevice, s));
           src = scratch;
+        }
+        if (l.kind == L_PROD) {
+          double2* pb = prodbuf + sh * shard_amps;
+          double2 scalar = make_double2(0.0, 0.0);
+          if (l.prod.last) {  // rank-bit factors: Pauli-basis weights, signs from the source shard's rank bits
+            const uint64_t src_rank = v.rank_bits ^ l.d.xglob;
+            for (const auto& zw : l.prod_z) {
+              const double2 w = __builtin_popcountll(src_rank & zw.first) & 1 ? make_double2(-zw.second.x, -zw.second.y)
+                                                                               : zw.second;
+              scalar = make_double2(scalar.x + w.x, scalar.y + w.y);
+            }
+            scalar = cm(l.prod_coeff, scalar);
+          }
+          launch_prod(d, l.prod, l.grid, l.smem, s, l.prod_first ? src : pb, pb, v.psi, v.lam, scalar, v.part);
+          ++launches;
+          continue;
         }
         if (l.kind == L_OBS_DIRECT) {
           launch_obs_direct(d, l.grid, s, v.psi, src, v.lam, dterms, v.part);
@@ -1784,10 +1957,21 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     return fail(SVG_EINVAL, ex.what());
   } catch (const CudaError& ex) {
     return fail(ex.code == cudaErrorMemoryAllocation ? SVG_ENOMEM : SVG_ECUDA, ex.what());
+  } catch (const JitFailure& ex) {
+    return fail(SVG_ECUDA, std::string("generated kernels: ") + ex.what());
+  } catch (const NcclError& ex) {
+    // a failed exchange leaves the peers mid-collective: abort the communicator so
+    // no rank blocks on it; the engine cannot run sharded sweeps afterwards
+    if (e->comm) {
+      const Nccl& nc = Nccl::get();
+      if (nc.comm_abort) nc.comm_abort(e->comm);
+      e->comm = nullptr;
+    }
+    return fail(SVG_ENCCL, ex.what());
   } catch (const std::bad_alloc&) {
     return fail(SVG_ENOMEM, "host allocation failed");
   } catch (const std::exception& ex) {
-    return fail(SVG_EINVAL, ex.what());
+    return fail(SVG_ECUDA, ex.what());
   }
 }
 
@@ -1905,6 +2089,7 @@ int svg_engine_destroy(svg_engine* e) {
   if (e->comm) Nccl::get().comm_destroy(e->comm);
   e->scratch.release();
   e->gathered.release();
+  e->prodbuf.release();
   e->psi.release();
   e->lam.release();
   e->partials.release();
@@ -1963,6 +2148,9 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "tile_fwd") {
     if (value < -1 || value > 13) return fail(SVG_EINVAL, "tile_fwd must be in [-1, 13]");
     e->opt_tile_fwd = value;
+  } else if (k == "low_qubits") {
+    if (value < 3 || value > 5) return fail(SVG_EINVAL, "low_qubits must be in [3, 5]");
+    e->opt_low_qubits = value;
   } else if (k == "scale_carry") {
     e->opt_scale_carry = value != 0;
   } else if (k == "free_lanes") {

@@ -124,6 +124,67 @@ __global__ void __launch_bounds__(kThreads) k_obs_pass(const double2* __restrict
   }
 }
 
+// Product-term pass (observable terms kept as products of 2x2 factors, e.g. the
+// letters H / + / - of hadamard_all; svgrad/observable.py:79-100 applies them
+// factor by factor with apply_matrix): the tile of `src` goes through this
+// pass's factors as butterflies in shared memory, then either to `dst` (the
+// product buffer, read by the next pass of the pipeline) or, on the last pass,
+// into lambda as scalar * tile with the energy partial <psi | scalar * tile>.
+__global__ void __launch_bounds__(kThreads) k_prod_pass(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                        const double2* __restrict__ psi, double2* __restrict__ lam,
+                                                        PassDesc d, const __grid_constant__ ProdFactors f,
+                                                        double2 scalar, double2* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t N = 1u << d.k;
+  double2* tile = reinterpret_cast<double2*>(smem_raw);
+  double2* wsum = tile + N;
+  uint64_t* hi = reinterpret_cast<uint64_t*>(wsum + kWarps);
+  build_hi(hi, d);
+  double2 e = make_double2(0.0, 0.0);
+  const uint64_t ntiles = 1ull << (d.n - d.k);
+  for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+    const uint64_t base = pdep64(T, d.rest);
+    __syncthreads();  // previous tile written out
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) tile[t] = src[gidx(base, t, hi, d.b)];
+    __syncthreads();
+    for (int j = 0; j < f.n; ++j) {
+      const uint32_t pos = f.pos[j];
+      const double2 m0 = f.m[j][0], m1 = f.m[j][1], m2 = f.m[j][2], m3 = f.m[j][3];
+      for (uint32_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        const uint32_t i0 = insert0(i, pos), i1 = i0 | (1u << pos);
+        const double2 v0 = tile[i0], v1 = tile[i1];
+        tile[i0] = cfma(m1, v1, cmul(m0, v0));
+        tile[i1] = cfma(m3, v1, cmul(m2, v0));
+      }
+      __syncthreads();
+    }
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
+      const uint64_t m = gidx(base, t, hi, d.b);
+      if (!f.last) {
+        dst[m] = tile[t];
+        continue;
+      }
+      const double2 val = cmul(scalar, tile[t]);
+      if (d.accumulate) {
+        const double2 old = lam[m];
+        lam[m] = make_double2(old.x + val.x, old.y + val.y);
+      } else {
+        lam[m] = val;
+      }
+      e = cjfma(psi[m], val, e);
+    }
+  }
+  e = warp_sum(e);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int w = 0; w < kWarps; ++w) s = make_double2(s.x + wsum[w].x, s.y + wsum[w].y);
+    partials[d.part_off + blockIdx.x] = s;
+  }
+}
+
 // Untiled observable pass for flip masks too wide for a tile: plain gathers.
 __global__ void __launch_bounds__(kThreads) k_obs_direct(const double2* __restrict__ psi,
                                                          const double2* __restrict__ src_state,
@@ -288,6 +349,9 @@ size_t obs_smem(int k, int b, int nterms) {
   return (sizeof(double2) << k) + sizeof(double2) * kWarps + sizeof(double2) * nterms +
          sizeof(uint32_t) * 2 * ((nterms + 1) & ~1) + (sizeof(uint64_t) << (k - b));
 }
+size_t prod_smem(int k, int b) {
+  return (sizeof(double2) << k) + sizeof(double2) * kWarps + (sizeof(uint64_t) << (k - b));
+}
 size_t rev_smem(int k, int b, int nslots) {
   return (2 * sizeof(double2) << k) + sizeof(double2) * kWarps * nslots + (sizeof(uint64_t) << (k - b));
 }
@@ -300,6 +364,7 @@ cudaError_t prepare_kernels(size_t max_smem) {
   cudaError_t e;
   if ((e = set_smem_attr(reinterpret_cast<const void*>(k_fwd_pass), max_smem)) != cudaSuccess) return e;
   if ((e = set_smem_attr(reinterpret_cast<const void*>(k_obs_pass), max_smem)) != cudaSuccess) return e;
+  if ((e = set_smem_attr(reinterpret_cast<const void*>(k_prod_pass), max_smem)) != cudaSuccess) return e;
   return set_smem_attr(reinterpret_cast<const void*>(k_rev_pass), max_smem);
 }
 
@@ -307,6 +372,7 @@ int occupancy(int which, size_t smem) {
   int blocks = 0;
   const void* fn = which == 0 ? reinterpret_cast<const void*>(k_fwd_pass)
                  : which == 1 ? reinterpret_cast<const void*>(k_obs_pass)
+                 : which == 3 ? reinterpret_cast<const void*>(k_prod_pass)
                               : reinterpret_cast<const void*>(k_rev_pass);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, smem);
   return blocks < 1 ? 1 : blocks;
@@ -319,6 +385,10 @@ void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double
 void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi, const double2* src,
                 double2* lam, const DevTerm* terms, double2* partials) {
   k_obs_pass<<<grid, kThreads, smem, s>>>(psi, src, lam, d, terms, partials);
+}
+void launch_prod(const PassDesc& d, const ProdFactors& f, int grid, size_t smem, cudaStream_t s, const double2* src,
+                 double2* dst, const double2* psi, double2* lam, double2 scalar, double2* partials) {
+  k_prod_pass<<<grid, kThreads, smem, s>>>(src, dst, psi, lam, d, f, scalar, partials);
 }
 void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, const double2* src,
                        double2* lam, const DevTerm* terms, double2* partials) {

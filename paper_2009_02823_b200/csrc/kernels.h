@@ -11,13 +11,16 @@ namespace svgb {
 size_t fwd_smem(int k, int b);
 size_t obs_smem(int k, int b, int nterms);
 size_t rev_smem(int k, int b, int nslots);
+size_t prod_smem(int k, int b);
 cudaError_t prepare_kernels(size_t max_smem);
-int occupancy(int which /*0 fwd, 1 obs, 2 rev*/, size_t smem);
+int occupancy(int which /*0 fwd, 1 obs, 2 rev, 3 product term*/, size_t smem);
 
 void launch_fwd(const PassDesc& d, int grid, size_t smem, cudaStream_t s, double2* psi,
                 const DevOp* ops, const double2* coef);
 void launch_obs(const PassDesc& d, int grid, size_t smem, cudaStream_t s, const double2* psi, const double2* src,
                 double2* lam, const DevTerm* terms, double2* partials);
+void launch_prod(const PassDesc& d, const ProdFactors& f, int grid, size_t smem, cudaStream_t s, const double2* src,
+                 double2* dst, const double2* psi, double2* lam, double2 scalar, double2* partials);
 void launch_obs_direct(const PassDesc& d, int grid, cudaStream_t s, const double2* psi, const double2* src,
                        double2* lam, const DevTerm* terms, double2* partials);
 // qubit swap of a sharded state (virtual shards in one allocation): for every

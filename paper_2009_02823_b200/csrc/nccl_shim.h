@@ -11,6 +11,11 @@
 
 namespace svgb {
 
+// NCCL failures (status SVG_ENCCL at the C-ABI, RuntimeError in Python)
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 struct NcclUniqueId {
   char internal[128];
 };
@@ -22,6 +27,7 @@ struct Nccl {
   using GetUniqueIdFn = int (*)(NcclUniqueId*);
   using CommInitRankFn = int (*)(NcclComm*, int, NcclUniqueId, int);
   using CommDestroyFn = int (*)(NcclComm);
+  using CommAbortFn = int (*)(NcclComm);
   using SendFn = int (*)(const void*, size_t, int, int, NcclComm, cudaStream_t);
   using RecvFn = int (*)(void*, size_t, int, int, NcclComm, cudaStream_t);
   using GroupFn = int (*)();
@@ -31,6 +37,7 @@ struct Nccl {
   GetUniqueIdFn get_unique_id = nullptr;
   CommInitRankFn comm_init_rank = nullptr;
   CommDestroyFn comm_destroy = nullptr;
+  CommAbortFn comm_abort = nullptr;
   SendFn send = nullptr;
   RecvFn recv = nullptr;
   GroupFn group_start = nullptr;
@@ -45,7 +52,7 @@ struct Nccl {
 
   void check(int rc, const char* what) const {
     if (rc != kNcclSuccess)
-      throw std::runtime_error(std::string(what) + ": " + (error_string ? error_string(rc) : "nccl error"));
+      throw NcclError(std::string(what) + ": " + (error_string ? error_string(rc) : "nccl error"));
   }
 
  private:
@@ -54,15 +61,16 @@ struct Nccl {
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's NCCL (torch) first
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) throw std::runtime_error("libnccl.so.2 not found");
+    if (!h) throw NcclError("libnccl.so.2 not found");
     auto sym = [&](const char* name) {
       void* f = dlsym(h, name);
-      if (!f) throw std::runtime_error(std::string("NCCL symbol missing: ") + name);
+      if (!f) throw NcclError(std::string("NCCL symbol missing: ") + name);
       return f;
     };
     n.get_unique_id = reinterpret_cast<GetUniqueIdFn>(sym("ncclGetUniqueId"));
     n.comm_init_rank = reinterpret_cast<CommInitRankFn>(sym("ncclCommInitRank"));
     n.comm_destroy = reinterpret_cast<CommDestroyFn>(sym("ncclCommDestroy"));
+    n.comm_abort = reinterpret_cast<CommAbortFn>(sym("ncclCommAbort"));
     n.send = reinterpret_cast<SendFn>(sym("ncclSend"));
     n.recv = reinterpret_cast<RecvFn>(sym("ncclRecv"));
     n.group_start = reinterpret_cast<GroupFn>(sym("ncclGroupStart"));

@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _native as N
 from .ir import NonInvertibleGateError, SIGMA, bound_matrix, derivative_scale, invert_small, kind_name, matrix_derivative
-from .operators import pauli_masks, pauli_strings
+from .operators import FACTOR_MATRICES, pauli_masks, pauli_strings, split_terms
 
 GATE_DTYPE = np.dtype(  # itemsize 816 = 51 complex128 slots (bind scatters into a flat complex view)
     [
@@ -51,6 +51,8 @@ TERM_DTYPE = np.dtype(
     [("coeff", "<c16"), ("x_mask", "<u8"), ("z_mask", "<u8"), ("n_y", "<i4"), ("reserved", "<i4")],
     align=True,
 )
+PRODUCT_DTYPE = np.dtype([("coeff", "<c16"), ("first_factor", "<i4"), ("num_factors", "<i4")], align=True)
+FACTOR_DTYPE = np.dtype([("qubit", "<i4"), ("reserved", "<i4"), ("m", "<c16", (4,))], align=True)
 _PAULI_FIXED = {"X": SIGMA["X"], "Y": SIGMA["Y"], "Z": SIGMA["Z"]}
 FLAG_REAL_SUMS = 1  # SVG_FLAG_REAL_SUMS: only 2*Re(sums) is consumed (Hermitian observables)
 FLAG_INPUT_LOCAL = 2  # SVG_FLAG_INPUT_LOCAL: input_amps is this rank's shard slice (state.ShardSlice)
@@ -206,26 +208,43 @@ def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     return gates, derivs
 
 
-def _lower_terms(obs) -> np.ndarray:
-    strings = pauli_strings(obs)
+def _lower_terms(obs):
+    """(Pauli-string table, product-term table, factor table) of an observable:
+    terms with at most a few H/+/- letters are expanded into Pauli strings, wider
+    ones stay products of 2x2 factors (operators.split_terms)."""
+    pauli_terms, products = split_terms(obs)
+    strings = pauli_strings(type("T", (), {"terms": pauli_terms})()) if pauli_terms else []
     terms = np.zeros(len(strings), dtype=TERM_DTYPE)
     for i, s in enumerate(strings):
         terms[i] = (s.coeff, s.x_mask, s.z_mask, s.n_y, 0)
-    return terms
+    nf = sum(sum(ch != "I" for ch in f) for _, f in products)
+    prods = np.zeros(len(products), dtype=PRODUCT_DTYPE)
+    factors = np.zeros(nf, dtype=FACTOR_DTYPE)
+    j = 0
+    for i, (c, f) in enumerate(products):
+        first = j
+        for q, ch in enumerate(f):
+            if ch != "I":
+                factors[j] = (q, 0, FACTOR_MATRICES[ch].reshape(-1))
+                j += 1
+        prods[i] = (complex(c), first, j - first)
+    return terms, prods, factors
 
 
 _TERMS_CACHE: dict = {}
 
 
-def lower_terms(obs) -> np.ndarray:
-    """Pauli-expanded term table, cached per observable terms object (terms are
-    immutable tuples: a repeated gradient call on the same observable reuses it)."""
+def lower_terms(obs):
+    """(Pauli strings, product terms, factors) tables, cached per observable terms
+    object (terms are immutable tuples: a repeated gradient call on the same
+    observable reuses them)."""
     terms_obj = obs.terms
     hit = _TERMS_CACHE.get(id(terms_obj))
     if hit is not None and hit[0] is terms_obj and hit[1] == obs.num_qubits:
         return hit[2]
     table = _lower_terms(obs)
-    table.setflags(write=False)
+    for a in table:
+        a.setflags(write=False)
     if isinstance(terms_obj, tuple):
         if len(_TERMS_CACHE) > 64:
             _TERMS_CACHE.clear()
@@ -238,7 +257,7 @@ class Problem:
 
     def __init__(self, circuit, params, obs, input_state, real_sums: bool = False):
         self.gates, self.derivs = bind(circuit, params)
-        self.terms = lower_terms(obs)
+        self.terms, self.products, self.factors = lower_terms(obs)
         self.num_derivs = len(self.derivs)
         from .state import basis_index_of
 
@@ -259,6 +278,10 @@ class Problem:
         p.gates = self.gates.ctypes.data_as(C.POINTER(N.svg_gate))
         p.derivs = self.derivs.ctypes.data_as(C.POINTER(N.svg_deriv))
         p.terms = self.terms.ctypes.data_as(C.POINTER(N.svg_pauli_term))
+        p.num_product_terms = len(self.products)
+        p.num_factors = len(self.factors)
+        p.product_terms = self.products.ctypes.data_as(C.POINTER(N.svg_product_term))
+        p.factors = self.factors.ctypes.data_as(C.POINTER(N.svg_factor))
         p.input_basis = 0 if basis is None else basis
         p.input_amps = None if self.amps is None else self.amps.ctypes.data
         self.c = p

@@ -5,9 +5,11 @@
 position j acting on qubit j; ``is_hermitian`` uses the same structural rule
 and the same dense fallback for at most 10 qubits.
 
-For the device every term is lowered to Pauli strings
-``(c, x_mask, z_mask, n_y)``: ``H = (X+Z)/sqrt2``, ``+ = (X - iY)/2``,
-``- = (X + iY)/2`` expand a term with w such letters into 2^w Pauli strings.
+For the device a term is lowered to Pauli strings ``(c, x_mask, z_mask,
+n_y)`` -- ``H = (X+Z)/sqrt2``, ``+ = (X - iY)/2``, ``- = (X + iY)/2`` expand
+a term with w such letters into 2^w strings -- when w <= 3, and otherwise kept
+as a product of 2x2 factor matrices (product-term passes on the device, e.g.
+the paper's benchmark operator ``hadamard_all`` as Walsh-Hadamard butterflies).
 A Pauli string P acts as ``(P psi)[m] = i^{n_y} (-1)^{popcount((m^x) & z)} psi[m ^ x]``
 with ``x`` = qubits holding X or Y and ``z`` = qubits holding Z or Y.
 """
@@ -40,7 +42,11 @@ _EXPANSION = {
     "+": ((0.5, "X"), (-0.5j, "Y")),
     "-": ((0.5, "X"), (0.5j, "Y")),
 }
-MAX_EXPANDED_TERMS = 1 << 16
+# Terms with more than this many H/+/- letters stay products of 2x2 factors on
+# the device (product-term passes: Walsh-Hadamard butterflies for H) instead of
+# 2^w Pauli strings; the observable passes share one partner load per flip mask,
+# so a few strings are cheaper than a product pipeline's extra state passes.
+MAX_EXPANDED_LETTERS = 3
 
 
 @dataclass(frozen=True)
@@ -133,8 +139,18 @@ def pauli_masks(letters: str) -> tuple[int, int, int]:
     return x, z, ny
 
 
-def pauli_strings(obs, limit: int = MAX_EXPANDED_TERMS) -> list[PauliString]:
-    """Expand every term into Pauli strings, in term order (no merging)."""
+def split_terms(obs, max_letters: int = MAX_EXPANDED_LETTERS):
+    """(terms for the Pauli expansion, terms kept as 2x2-factor products), in term order."""
+    pauli, prods = [], []
+    for coeff, factors in obs.terms:
+        wide = sum(ch in "H+-" for ch in factors) > max_letters
+        (prods if wide else pauli).append((complex(coeff), factors))
+    return tuple(pauli), tuple(prods)
+
+
+def pauli_strings(obs, limit: int | None = None) -> list[PauliString]:
+    """Expand every term into Pauli strings, in term order (no merging).
+    ``limit``: refuse expansions wider than this (None: no limit)."""
     out: list[PauliString] = []
     for coeff, factors in obs.terms:
         coeff = complex(coeff)
@@ -145,11 +161,8 @@ def pauli_strings(obs, limit: int = MAX_EXPANDED_TERMS) -> list[PauliString]:
         width = 1
         for c in choices:
             width *= len(c)
-        if len(out) + width > limit:
-            raise NotImplementedError(
-                f"term {factors!r} expands to {width} Pauli strings (limit {limit}); "
-                "product-term observables this wide are not lowered yet"
-            )
+        if limit is not None and len(out) + width > limit:
+            raise ValueError(f"term {factors!r} expands to {width} Pauli strings (limit {limit})")
         for combo in product(*choices):
             w = coeff
             for weight, _ in combo:

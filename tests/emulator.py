@@ -75,6 +75,40 @@ def _generator(vec, gate, kvec, rank_bits=0):
     return np.where(((idx | rank_bits) & ctrl) == ctrl, out, 0)
 
 
+def _rank_pauli_parts(m, bit):
+    """2x2 factor on a rank bit in the Pauli basis: [(x, z, weight incl. i^n_y)] (engine.cu lowering)."""
+    m = np.asarray(m).reshape(2, 2)
+    a, d = (m[0, 0] + m[1, 1]) / 2, (m[0, 0] - m[1, 1]) / 2
+    b, c = (m[0, 1] + m[1, 0]) / 2, 1j * (m[0, 1] - m[1, 0]) / 2
+    return [(0, 0, a), (bit, 0, b), (bit, bit, c * 1j), (0, bit, d)]
+
+
+def _product_terms(prob, psi, l2p=None, nloc=None, rank=0, fetch=None):
+    """sum_t c_t (x)F_t psi over the problem's product terms (dense factor-by-factor
+    application; rank-bit factors in Pauli form with partner shards from ``fetch``)."""
+    out = np.zeros_like(psi)
+    nloc = nloc if nloc is not None else int(np.log2(psi.size))
+    for pt in prob.products:
+        facs = prob.factors[int(pt["first_factor"]): int(pt["first_factor"]) + int(pt["num_factors"])]
+        loc, subs = [], [(0, 0, 1.0 + 0j)]
+        for f in facs:
+            q = int(f["qubit"]) if l2p is None else l2p[int(f["qubit"])]
+            if q < nloc:
+                loc.append((q, f["m"]))
+                continue
+            subs = [(x | x2, z | z2, w * w2) for x, z, w in subs for x2, z2, w2 in _rank_pauli_parts(f["m"], 1 << q)
+                    if w * w2 != 0]
+        for x, z, w in subs:
+            src = psi if x == 0 else fetch(x)
+            v = src.copy()
+            for q, m in loc:
+                v = _mat_apply(v, m, [q], 0)
+            src_rank = (rank << nloc) ^ x
+            sign = -1.0 if bin(src_rank & z).count("1") & 1 else 1.0
+            out += complex(pt["coeff"]) * w * sign * v
+    return out
+
+
 def emulate(circuit, params, obs, input_state, tile_qubits=0, sms=0):
     """(sums complex[P], energy, pass_count) computed from the lowered tables."""
     prob = Problem(circuit, np.asarray(params, dtype=float), obs, input_state)
@@ -87,6 +121,7 @@ def emulate(circuit, params, obs, input_state, tile_qubits=0, sms=0):
     lam = np.zeros_like(psi)
     for t in terms:
         lam += _pauli_apply(psi, 0.0, t["coeff"], int(t["x_mask"]), int(t["z_mask"]), int(t["n_y"]), 0)
+    lam += _product_terms(prob, psi)
     energy = np.vdot(psi, lam)
     first = np.concatenate([[0], np.cumsum(gates["nderiv"])]).astype(int)
     contrib = np.zeros(len(derivs), dtype=complex)
@@ -185,6 +220,13 @@ def emulate_sharded(circuit, params, obs, input_state, world, rank, exchange, ti
                 fetched[xg] = exchange(psi, rank ^ (xg >> nloc))
             src = fetched[xg]
         lam += _pauli_apply(psi, 0.0, t["coeff"], x & loc, z, int(t["n_y"]), 0, rank_bits, src, rank_bits ^ xg)
+
+    def fetch(xg):
+        if xg not in fetched:
+            fetched[xg] = exchange(psi, rank ^ (xg >> nloc))
+        return fetched[xg]
+
+    lam += _product_terms(prob, psi, l2p, nloc, rank, fetch)
     energy = np.vdot(psi, lam)
     first = np.concatenate([[0], np.cumsum(gates["nderiv"])]).astype(int)
     contrib = np.zeros(len(derivs), dtype=complex)

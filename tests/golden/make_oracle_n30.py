@@ -3,6 +3,7 @@
     python tests/golden/make_oracle_n30.py cfg4        # BASELINE cfg 4 at its full size (n = 30)
     python tests/golden/make_oracle_n30.py cfg5_n30    # cfg 5's structure (12 layers RX/RY/RZ + RZZ chain,
                                                        # 128 random Pauli strings) at n = 30
+    python tests/golden/make_oracle_n30.py hadamard_n26  # cfg 4's structure at n = 26 under hadamard_all
 
 The reference needs ~0.5 TiB and ~5 h for cfg 4 and cannot hold cfg 5 at all
 (SURVEY.md §8(c)), so these fixtures come from the C oracle
@@ -34,19 +35,29 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(HERE))
 
-from golden.make_golden import circuit_digest, obs_digest  # noqa: E402
+from golden.digest import circuit_digest, obs_digest  # noqa: E402
 
-CASES = {"cfg4": (4, None), "cfg5_n30": (5, 30)}
+# name -> (config, qubits, observable override): hadamard_n26 is cfg 4's circuit structure at
+# n = 26 under the paper's benchmark operator hadamard_all (one product term of 26 H factors)
+CASES = {"cfg4": (4, None, None), "cfg5_n30": (5, 30, None), "hadamard_n26": (4, 26, "hadamard_all")}
+
+
+def workload(name):
+    import paper_2009_02823_b200 as sv
+
+    cfg, n, obs = CASES[name]
+    w = sv.build_workload(cfg, n)
+    if obs:
+        w = type(w)(w.cfg, w.num_qubits, w.circuit, sv.builtin_observable(obs, w.num_qubits), w.theta)
+    return w
 
 
 def main():
     name = sys.argv[1]
     threads = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    cfg, n = CASES[name]
-    import paper_2009_02823_b200 as sv
     from oracle import oracle
 
-    w = sv.build_workload(cfg, n)
+    w = workload(name)
     with open(oracle.SRC, "rb") as f:
         src_sha = hashlib.sha256(f.read()).hexdigest()
     t0 = time.perf_counter()

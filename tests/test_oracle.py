@@ -101,18 +101,19 @@ def test_n30_fixtures_are_pinned_to_this_oracle():
     import json
     import os
 
-    import paper_2009_02823_b200 as sv
-    from golden.make_golden import circuit_digest, obs_digest
+    from golden.digest import circuit_digest, obs_digest
 
     here = os.path.join(os.path.dirname(__file__), "golden")
     found = 0
-    for name, (cfg, n) in {"cfg4": (4, None), "cfg5_n30": (5, 30)}.items():
+    from golden.make_oracle_n30 import CASES, workload
+
+    for name in CASES:
         path = os.path.join(here, f"oracle_{name}.json")
         if not os.path.exists(path):
             continue
         found += 1
         rec = json.load(open(path))["cases"][name]
-        w = sv.build_workload(cfg, n)
+        w = workload(name)
         assert rec["circuit_digest"] == circuit_digest(w.circuit)
         assert rec["obs_digest"] == obs_digest(w.observable)
         assert rec["theta_sum"] == pytest.approx(float(np.sum(w.theta)), abs=0)
