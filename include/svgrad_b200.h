@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SVG_ABI_VERSION 2
+#define SVG_ABI_VERSION 3
 #define SVG_MAX_QUBITS 40
 
 typedef struct { double re, im; } svg_c128;
@@ -168,6 +168,10 @@ typedef struct {
   int64_t exchange_bytes;    /* sharded engines: bytes one shard sends to partners per sweep */
   double ms_host_lower;      /* host time: validation + lowering (plans, op tables, kernel lookup) */
   double ms_host_prep;       /* host time: staging buffers between lowering and the first launch */
+  /* ABI 3: numeric guard -- device sums (per-shard finalized partials of every
+   * derivative slot and the energy) that came out NaN or infinite */
+  int32_t nonfinite;
+  int32_t reserved;
 } svg_stats;
 
 typedef struct svg_engine svg_engine;

@@ -18,6 +18,7 @@ from .adjoint import (
     circuit_expectation,
     finite_difference_gradient,
     non_hermitian_gradient,
+    reference_gradient,
     reverse_mode_gradient,
     sweep,
 )

@@ -49,14 +49,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
             assert ")SVGB\"" not in text
             f.write(f'static const char {name}[] = R"SVGB({text})SVGB";\n')
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", os.path.join(ROOT, "include"), "-I", tmp]
+    headers = [d for d in deps if not d.endswith((".cu", ".cpp"))]
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(tmp, src + ".o")
+        objs.append(obj)
+        if not force and not _stale(obj, [os.path.join(CSRC, src), *headers]):
+            continue  # incremental: object newer than its source and every header
         cmd = [nvcc(), *ARCH, *common, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-g", "-I", os.path.join(ROOT, "include"),
                    "-c", os.path.join(CSRC, src), "-o", obj]
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        cmds.append(cmd)
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for fut in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
+            fut.result()
     tmp_lib = LIB + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp_lib, *objs, "-lcudart", "-ldl"], check=True)
     os.replace(tmp_lib, LIB)

@@ -11,7 +11,7 @@ import os
 import threading
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvgb200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 SVG_OK, SVG_EINVAL, SVG_ENOMEM, SVG_ECUDA, SVG_ENCCL, SVG_EUNSUPPORTED = range(6)
 FORM_PAULI, FORM_MAT = 0, 1
@@ -86,7 +86,8 @@ class svg_stats(C.Structure):
         ("tile_qubits", C.c_int32), ("pass_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64), ("segments", C.c_int32), ("reg_bits", C.c_int32),
         ("swaps", C.c_int32), ("jit_passes", C.c_int32), ("exchange_bytes", C.c_int64),
-        ("ms_host_lower", C.c_double), ("ms_host_prep", C.c_double),
+        ("ms_host_lower", C.c_double), ("ms_host_prep", C.c_double), ("nonfinite", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -1906,6 +1906,11 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         tot[i].y += hres[r * cnt + i].y;
       }
 
+    // numeric guard: a non-finite partial makes its finalized sum non-finite
+    int32_t nonfinite = 0;
+    for (int r = 0; r < nres; ++r)
+      for (int64_t i = 0; i < cnt; ++i)
+        nonfinite += !(std::isfinite(hres[r * cnt + i].x) && std::isfinite(hres[r * cnt + i].y));
     const int A = with_reverse ? p->num_derivs : 0;
     if (energy_out) *energy_out = svg_c128{tot[A].x, tot[A].y};
     if (with_reverse) {
@@ -1951,6 +1956,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       stats->jit_passes = jit_launches;
       stats->ms_host_lower = std::chrono::duration<double, std::milli>(t_lowered - t_enter).count();
       stats->ms_host_prep = std::chrono::duration<double, std::milli>(t_launch - t_lowered).count();
+      stats->nonfinite = nonfinite;
     }
     return SVG_OK;
   } catch (const InvalidArg& ex) {

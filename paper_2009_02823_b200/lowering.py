@@ -148,8 +148,12 @@ def _put(block: np.ndarray, m: np.ndarray) -> None:
     block[: flat.size] = flat
 
 
-def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-    """Gate and derivative tables for one theta (raises NonInvertibleGateError)."""
+def bind(circuit, params: np.ndarray, forward_only: bool = False) -> tuple[np.ndarray, np.ndarray]:
+    """Gate and derivative tables for one theta (raises NonInvertibleGateError).
+
+    ``forward_only``: the tables feed a forward sweep only (expectation), which never
+    rewinds -- a singular NonUnitary gate is accepted there, as in the reference's
+    forward-only paths (svgrad/gradients.py:201-237, 262-294)."""
     st = _structure(circuit)
     # per-thread working tables, reused across calls (every theta-dependent field
     # is rewritten below; the rest is structure): no 100s-of-KB copy per call
@@ -192,7 +196,9 @@ def bind(circuit, params: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
                 try:
                     rew = invert_small(m)
                 except ValueError as exc:
-                    raise NonInvertibleGateError(f"non-invertible gate {i}: {exc}") from exc
+                    if not forward_only:
+                        raise NonInvertibleGateError(f"non-invertible gate {i}: {exc}") from exc
+                    rew = adj  # never read: no rewind in a forward sweep
             else:
                 rew = adj
             _put(gates["fwd"][i], m)
@@ -255,8 +261,8 @@ def lower_terms(obs):
 class Problem:
     """Owns the numpy tables and the svg_problem that points into them."""
 
-    def __init__(self, circuit, params, obs, input_state, real_sums: bool = False):
-        self.gates, self.derivs = bind(circuit, params)
+    def __init__(self, circuit, params, obs, input_state, real_sums: bool = False, forward_only: bool = False):
+        self.gates, self.derivs = bind(circuit, params, forward_only)
         self.terms, self.products, self.factors = lower_terms(obs)
         self.num_derivs = len(self.derivs)
         from .state import basis_index_of

@@ -56,6 +56,13 @@ CLI_CASES = [
     ("qubits 2\nparams 2\nry q0 p0\nrp zx q0 q1 p1\nh q1\n", "obs:qubits 2\n0.5 0.0 XZ\n0.0 0.7 +Y\n", "0.4,-1.1",
      "reverse"),
     ("qubits 2\nparams 1\nry q3 p0\n", "z_all", "0.1", "reverse"),
+    # the O(P^2) reference schedule (svgrad/cli.py:79-89): counters G + A(G-1) / A+1 clones
+    ("qubits 1\nparams 1\nry q0 p0\n", "z_all", "0.3", "reference"),
+    ("qubits 3\nparams 4\nrx q0 p0\nry q1 p1\ncx q0 q2\ncrz q1 q2 p2\nphase q0 p3\nrz q2 p1\n", "hadamard_all",
+     "0.3,1.2,-0.7,2.2", "reference"),
+    ("qubits 3\nparams 3\nry q0 p0\ncry q0 q1 p1\nrp xy q1 q2 p2\nh q2\n", "hadamard_all", "0.9,-0.4,1.7", "reference"),
+    ("qubits 2\nparams 2\nry q0 p0\nrp zx q0 q1 p1\nh q1\n", "obs:qubits 2\n0.5 0.0 XZ\n0.0 0.7 +Y\n", "0.4,-1.1",
+     "reference"),
 ]
 
 

@@ -120,3 +120,32 @@ def test_reverse_mode_time_is_linear_in_parameters():
         ts.append(best)
     slope = np.polyfit(np.log(ps), np.log(ts), 1)[0]
     assert 0.75 <= slope <= 1.35, (slope, ts)
+
+
+@pytest.mark.parametrize("name", ["single_ry_3", "family_A4_1", "family_D5_0", "repeated_rz", "unreferenced_slot",
+                                  "no_params", "multi_param_fd", "shared_slot", "non_unitary", "all_kinds_4_random",
+                                  "all_kinds_6_basis", "random_input_family_C", "cfg1"])
+def test_reference_gradient_quadratic_schedule(name):
+    """The reference's O(P^2) schedule on the GPU (svgrad/gradients.py:201-237, one
+    derivative-inserted forward sweep per parameter occurrence) against the reference's
+    reverse-mode outputs (the reference pins reverse == reference to 1e-11,
+    pkg/tests/test_gradients.py:131-144), with the quadratic counters
+    (pkg/tests/test_gradients.py:324-333)."""
+    from cases import small_cases
+
+    rec = load_golden()[name]
+    circ, theta, obs, inp, _ = materialize({**small_cases(), **config_cases()}[name])
+    rep = sv.reference_gradient(circ, theta, obs, inp)
+    assert max_err(rep.values, cvec(rec["values"])) <= 1e-10
+    assert abs(rep.energy - complex(*rec["energy"])) <= 1e-12
+    G = len(circ.gates)
+    A = sum(len(g.param_refs) for g in circ.gates)
+    assert vars(rep.counters) == {"gate_applies": G + A * (G - 1), "derivative_applies": A, "clones": A + 1,
+                                  "inner_products": A, "observable_applies": 1}
+
+
+def test_reference_gradient_rejects_non_hermitian():
+    circ = sv.Circuit(1, (sv.ry(0, 0),), 1)
+    obs = sv.Observable(1, ((1.0, "+"),))
+    with pytest.raises(ValueError, match="non_hermitian_gradient"):
+        sv.reference_gradient(circ, [0.1], obs, sv.init_basis_state(1))

@@ -137,3 +137,22 @@ def test_generated_kernels_compile_for_sm100a(cfg, n, tile):
         pytest.skip("libnvrtc not present")
     assert rc == 0, lib.svg_last_error()
     assert count.value > 0
+
+
+def test_numeric_guard_rules():
+    """NaN/Inf device sums: raise only when the inputs cannot explain them (finite
+    tables and input, unitary gates); otherwise pass them through as numpy would."""
+    from paper_2009_02823_b200.adjoint import _numeric_guard
+    from paper_2009_02823_b200.lowering import Problem
+
+    w = sv.build_workload(1, 6)
+    pr = Problem(w.circuit, w.theta, w.observable, sv.BasisState(6))
+    with pytest.raises(FloatingPointError, match="device fault"):
+        _numeric_guard(w.circuit, pr, 3)
+    theta = w.theta.copy()
+    theta[2] = np.nan
+    pr_nan = Problem(w.circuit, theta, w.observable, sv.BasisState(6))
+    _numeric_guard(w.circuit, pr_nan, 3)  # NaN input: the reference propagates it too
+    nu = sv.Gate(sv.NonUnitary(lambda: np.diag([1e300, 1.0]), 0), (0,))
+    circ = sv.Circuit(6, (*w.circuit.gates, nu), w.circuit.num_params)
+    _numeric_guard(circ, Problem(circ, w.theta, w.observable, sv.BasisState(6)), 1)  # may overflow: allowed
