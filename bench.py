@@ -73,13 +73,8 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tile-qubits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0, help="reverse register tile: 2^bits amplitudes/thread (3/4)")
-    ap.add_argument("--reg-bits-fwd", type=int, default=0, help="forward register tile: 2^bits amplitudes/thread")
-    ap.add_argument("--no-stage", action="store_true", help="generated kernels: no cp.async next-tile staging")
-    ap.add_argument("--no-pdl", action="store_true", help="generated kernels: no programmatic dependent launch")
-    ap.add_argument("--no-fuse-diag", action="store_true", help="generated kernels: no fused diagonal runs")
     ap.add_argument("--jit", type=int, default=1, help="circuit-specialised kernels: 0 off, 1 auto, 2 always")
     ap.add_argument("--opt", action="append", default=[], help="extra engine option KEY=VALUE (repeatable)")
-    ap.add_argument("--jit-blocks", type=str, default="0,0", help="generated kernels: min CTAs/SM fwd,rev (0 default)")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one state over the ranks (default for cfg 4/5)")
     ap.add_argument("--max-gates", type=int, default=0, help="gates per pass cap (0: planner default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -355,16 +350,8 @@ def _configure(eng, args):
     eng.set_option("tile_qubits", args.tile_qubits)
     if args.reg_bits:
         eng.set_option("reg_bits", args.reg_bits)
-    if args.reg_bits_fwd:
-        eng.set_option("reg_bits_fwd", args.reg_bits_fwd)
-    eng.set_option("stage", 0 if args.no_stage else 1)
-    eng.set_option("pdl", 0 if args.no_pdl else 1)
-    eng.set_option("fuse_diag", 0 if args.no_fuse_diag else 1)
     eng.set_option("jit", args.jit)
     eng.set_option("max_gates_per_pass", args.max_gates)
-    jb = [int(x) for x in args.jit_blocks.split(",")]
-    eng.set_option("jit_blocks_fwd", jb[0])
-    eng.set_option("jit_blocks_rev", jb[1])
     for kv in args.opt:
         key, val = kv.split("=")
         eng.set_option(key, int(val))

@@ -194,31 +194,15 @@ struct svg_engine {
   size_t max_smem_sm = 233472;  // shared memory per SM (B200: 228 KB)
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 0, opt_reg_bits_fwd = 0, opt_prefetch = 0;  // reg bits 0: auto
+  int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 0;  // reg bits 0: auto
   // virtual engines: run the NCCL-mode data path (half-shard pack -> copy ->
   // unpack, partner fetch into scratch) with device copies as the transport
   int64_t opt_emulate_transport = 0;
   // circuit-specialised register-tile kernels (jit.cu): 0 off, 1 auto (shards of
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
-  int64_t opt_stage = 1;  // generated kernels: stage the next tile with cp.async
-  int64_t opt_pdl = 1;    // generated kernels: programmatic dependent launch
-  int64_t opt_fuse_diag = 1;  // generated reverse kernels: fused runs of diagonal rotations
-  int64_t opt_acc_prefetch = 1;  // generated reverse kernels: accumulator loads ahead of the op
-  int64_t opt_free_lanes = 1;    // generated kernels: free-lane segment plans where cheaper
-  int64_t opt_scale_carry = 1;   // generated kernels: deferred scale carried across layout changes
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
   int64_t opt_low_qubits = 3;    // generated kernels: contiguous low qubits every tile holds (3..5)
-  int64_t opt_early_fwd = 1;     // one shard: launch the forward passes while the rest is lowered
-  int64_t opt_direct_store = 0;  // free-lane passes store from a non-global lane layout (no final transpose)
-  int64_t opt_early_stage = 0;   // reverse passes: stage the next tile's phi at tile start
-  int64_t opt_lane_cost10 = 37, opt_xpose_cost10 = 53;  // plan cost model (reverse; register op = 10)
-  int64_t opt_fwd_lane_cost10 = 50, opt_fwd_xpose_cost10 = 80;  // forward passes (one buffer)
-  int64_t opt_jit_blocks_fwd = 0, opt_jit_blocks_rev = 0;  // generated kernels: min CTAs per SM (0: default)
-  // reverse passes: shared-memory budget (KB) of the lane-group inner-product
-  // accumulators; 0 = auto (interpreter 24 KB; generated kernels: whatever the
-  // CTA's share of the SM leaves next to its tile buffers)
-  int64_t opt_acc_kb = 0;
   mutable std::string jit_error;
   bool jit_dry_run = false;        // svg_debug_jit_check
   mutable int jit_dry_count = 0;
@@ -508,6 +492,11 @@ constexpr int kRegPassGates = 40;
 // States this large (per shard) stream HBM: generated kernels use 12-qubit tiles
 // (a narrower reverse tile gets a forward schedule over k+1-qubit tiles).
 constexpr int kWideTileQubits = 24;
+// Segment-plan cost model in register-op units (a register rotation = 1): a lane
+// flip is a warp shuffle of both buffers (forward: one), a layout change a
+// shared-memory transpose.  Measured with tools/pass_model.py (round 1).
+constexpr double kLaneCost = 3.7, kXposeCost = 5.3;        // reverse passes (phi and lambda)
+constexpr double kFwdLaneCost = 5.0, kFwdXposeCost = 8.0;  // forward passes (psi only)
 
 // One register op for gate g: operator coefficients `c` (a, b of a I + b P),
 // optionally fused with the post-gate generator `kpost` into `slot`.
@@ -724,7 +713,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // latency hiding when a pass is only a few tile rounds)
   const int Rauto = (nloc <= 23 && !jit_expected) ? 3 : 4;
   const int RB = e->opt_reg_bits ? static_cast<int>(e->opt_reg_bits) : Rauto;          // reverse passes
-  const int RF = e->opt_reg_bits_fwd ? static_cast<int>(e->opt_reg_bits_fwd) : Rauto;  // forward passes
+  const int RF = RB;  // forward passes
   L.R = RB;
   // thread count of a register-tile CTA: the interpreter's launch bounds, or 512
   // for the generated kernels (their launch bounds follow the thread count)
@@ -847,7 +836,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   std::vector<Swizzle> pswz(steps.size()), pswz_f(fsteps.size());
   // free-lane plans also need tile staging (a first segment off the global
   // layout reads its tile from the staged copy)
-  const bool free_lanes = jit_planned && e->opt_free_lanes && e->opt_stage;
+  const bool free_lanes = jit_planned;
   // segments of one pass at tile width kk with R register bits: the fixed-lane
   // plan, or the free-lane plan when the cost model prefers it (lc: lane op,
   // xc: layout change, in register-op units)
@@ -900,13 +889,13 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     // register-op units per amplitude: a lane flip is a warp shuffle of both (fwd:
     // one) buffers (4 SHFL per 16-byte amplitude at half the DFMA rate), a layout
     // change 32 B of shared-memory traffic per amplitude and buffer
-    const double lc = 0.1 * double(e->opt_lane_cost10), xc = 0.1 * double(e->opt_xpose_cost10);
+    const double lc = kLaneCost, xc = kXposeCost;
     for (size_t si = 0; si < steps.size(); ++si)
       if (!steps[si].swap) pass_segments(steps[si].pass, pgates[si], pshapes[si], L.k, RB, lc, xc, &psegs[si], &pswz[si]);
     for (size_t si = 0; si < fsteps.size(); ++si)
       if (!fsteps[si].swap)
-        pass_segments(fsteps[si].pass, fpgates[si], fpshapes[si], kf, RF, 0.1 * double(e->opt_fwd_lane_cost10),
-                      0.1 * double(e->opt_fwd_xpose_cost10), &psegs_f[si], &pswz_f[si]);
+        pass_segments(fsteps[si].pass, fpgates[si], fpshapes[si], kf, RF, kFwdLaneCost, kFwdXposeCost, &psegs_f[si],
+                      &pswz_f[si]);
   }
   auto reg_launch = [&](const Pass& ps, int nb, int kk) {
     Launch l;
@@ -931,7 +920,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
 
   // generated kernels keep the deferred scale C across layout changes (one
   // flush per tile, at the store) when a pass has no shared-memory segments
-  const bool carry = jit_planned && e->opt_scale_carry;
+  const bool carry = jit_planned;
   auto all_reg = [](const std::vector<Segment>& v) {
     for (const Segment& sg : v)
       if (!sg.reg) return false;
@@ -983,7 +972,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         }
         L.segs.push_back(sd);
       }
-      if (prev_l != ~0u && prev_l != 31u && !e->opt_direct_store) {  // back to the global lane layout for the store
+      if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
         SegLocal sl;
         SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, kf, RF, &sl);
         sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
@@ -1017,10 +1006,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.nloc = nloc;
         jp.threads = l.threads;
         jp.tiles = l.tiles;
-        jp.stage = e->opt_stage != 0;
-        jp.fuse_diag = e->opt_fuse_diag != 0;
-        jp.acc_prefetch = e->opt_acc_prefetch != 0;
-        jp.min_blocks = static_cast<int>(e->opt_jit_blocks_fwd);
         jp.rest = l.d.rest;
         jp.q = l.d.q;
         jp.swz = l.swz.col;
@@ -1308,7 +1293,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
           }
           L.segs.push_back(sd);
         }
-        if (prev_l != ~0u && prev_l != 31u && !e->opt_direct_store) {  // back to the global lane layout for the store
+        if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
           SegLocal sl;
           SegDesc sd = make_seg(SEG_REG, default_regs(RB), 31u, l.swz, L.k, RB, &sl);
           sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
@@ -1334,7 +1319,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // lane-group inner-product accumulators: combine 2^shift lanes so that the
   // shared accumulators stay within 24 KB (two 128-thread CTAs with 64 KB of
   // transpose tiles still fit an SM; no per-op full warp reductions)
-  const size_t acc_budget = size_t(e->opt_acc_kb ? e->opt_acc_kb : 24) << 10;
+  const size_t acc_budget = size_t(24) << 10;
   auto set_thread_acc = [acc_budget](Launch& l) {
     l.d.thread_acc = l.nb == 2 && l.d.nslots > 0;
     l.d.acc_shift = 0;
@@ -1430,13 +1415,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     passes.reserve(regl.size());
     for (Launch* l : regl) {
       set_thread_acc(*l);
-      if (l->d.thread_acc && e->opt_acc_kb == 0) {
+      if (l->d.thread_acc) {
         // auto budget: the SM's shared memory split over the kernel's CTAs per SM,
         // minus tile / staging buffers and per-warp accumulators.  Every halving
         // of the accumulators costs a butterfly step per op (measured: 40-slot
         // passes 8 % slower at shift 1 than at shift 0).
-        const int blocks = l->nb == 2 ? (e->opt_jit_blocks_rev ? int(e->opt_jit_blocks_rev) : std::max(1, std::min(2, 256 / l->threads)))
-                                      : (e->opt_jit_blocks_fwd ? int(e->opt_jit_blocks_fwd) : (l->R == 3 ? 2 : 4));
+        const int blocks = l->nb == 2 ? std::max(1, std::min(2, 256 / l->threads)) : (l->R == 3 ? 2 : 4);
         const size_t share = std::min<size_t>(e->max_smem, (size_t(e->max_smem_sm) / blocks) - 1024);
         const size_t fixed = (sizeof(double2) << l->d.k) * l->nb + sizeof(double2) * (l->threads / 32) * l->d.nslots;
         const size_t budget = share > fixed + 4096 ? share - fixed : 4096;
@@ -1454,15 +1438,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.thread_acc = l->d.thread_acc != 0;
       jp.acc_shift = l->d.acc_shift;
       jp.tiles = l->tiles;
-      jp.stage = e->opt_stage != 0;
-      jp.fuse_diag = e->opt_fuse_diag != 0;
-      jp.acc_prefetch = e->opt_acc_prefetch != 0;
-      jp.min_blocks = static_cast<int>(l->nb == 2 ? e->opt_jit_blocks_rev : e->opt_jit_blocks_fwd);
       jp.rest = l->d.rest;
       jp.q = l->d.q;
       jp.swz = l->swz.col;
       jp.scale_carry = carry;
-      jp.early_stage = e->opt_early_stage != 0;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -1600,7 +1579,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     // One shard: the initial state is set up before the lowering, and the forward
     // passes go out as soon as they are lowered (lower()'s fwd_ready), so the GPU
     // runs them while the host lowers the observable and the reverse sweep.
-    const bool early = e->shards_local == 1 && !e->comm && e->opt_early_fwd;
+    const bool early = e->shards_local == 1 && !e->comm;
     int64_t early_launches = 0;
     std::function<void(Lowered&)> fwd_cb;
     if (early) {
@@ -1626,7 +1605,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
           cfg.stream = e->stream;
           cudaLaunchAttribute attr[1];
           attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-          attr[0].val.programmaticStreamSerializationAllowed = e->opt_pdl ? 1 : 0;
+          attr[0].val.programmaticStreamSerializationAllowed = 1;
           cfg.attrs = attr;
           cfg.numAttrs = 1;
           void* params[] = {args.data()};
@@ -1756,7 +1735,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = e->opt_pdl ? 1 : 0;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       void* params[] = {args.data()};
@@ -2125,50 +2104,20 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     e->opt_tile = value;
   } else if (k == "profile") {
     e->opt_profile = value;
-  } else if (k == "reg_bits" || k == "reg_bits_fwd") {
+  } else if (k == "reg_bits") {
     if (value != 0 && value != 3 && value != 4) return fail(SVG_EINVAL, k + " must be 0 (auto), 3 or 4");
-    (k == "reg_bits" ? e->opt_reg_bits : e->opt_reg_bits_fwd) = value;
-  } else if (k == "prefetch") {  // accepted for compatibility; the bulk-copy tile prefetch was removed
-    e->opt_prefetch = value != 0;
+    e->opt_reg_bits = value;
   } else if (k == "emulate_transport") {
     e->opt_emulate_transport = value != 0;
   } else if (k == "kernel") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "kernel must be 0 (auto), 1 (shared-memory tiles) or 2 (register tiles)");
     e->opt_kernel = value;
-  } else if (k == "jit_blocks_fwd" || k == "jit_blocks_rev") {
-    if (value < 0 || value > 8) return fail(SVG_EINVAL, k + " must be in [0, 8]");
-    (k == "jit_blocks_fwd" ? e->opt_jit_blocks_fwd : e->opt_jit_blocks_rev) = value;
-  } else if (k == "acc_kb") {
-    if (value < 0 || value > 200) return fail(SVG_EINVAL, "acc_kb must be in [0 (auto), 200]");
-    e->opt_acc_kb = value;
-  } else if (k == "lane_cost10" || k == "xpose_cost10" || k == "fwd_lane_cost10" || k == "fwd_xpose_cost10") {
-    if (value < 1 || value > 1000) return fail(SVG_EINVAL, k + " must be in [1, 1000]");
-    (k == "lane_cost10" ? e->opt_lane_cost10 : k == "xpose_cost10" ? e->opt_xpose_cost10
-                                            : k == "fwd_lane_cost10" ? e->opt_fwd_lane_cost10 : e->opt_fwd_xpose_cost10) = value;
-  } else if (k == "early_stage") {
-    e->opt_early_stage = value != 0;
-  } else if (k == "direct_store") {
-    e->opt_direct_store = value != 0;
-  } else if (k == "early_fwd") {
-    e->opt_early_fwd = value != 0;
   } else if (k == "tile_fwd") {
     if (value < -1 || value > 13) return fail(SVG_EINVAL, "tile_fwd must be in [-1, 13]");
     e->opt_tile_fwd = value;
   } else if (k == "low_qubits") {
     if (value < 3 || value > 5) return fail(SVG_EINVAL, "low_qubits must be in [3, 5]");
     e->opt_low_qubits = value;
-  } else if (k == "scale_carry") {
-    e->opt_scale_carry = value != 0;
-  } else if (k == "free_lanes") {
-    e->opt_free_lanes = value != 0;
-  } else if (k == "acc_prefetch") {
-    e->opt_acc_prefetch = value != 0;
-  } else if (k == "fuse_diag") {
-    e->opt_fuse_diag = value != 0;
-  } else if (k == "pdl") {
-    e->opt_pdl = value != 0;
-  } else if (k == "stage") {
-    e->opt_stage = value != 0;
   } else if (k == "jit") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "jit must be 0 (off), 1 (auto) or 2 (always)");
     e->opt_jit = value;
@@ -2241,8 +2190,6 @@ extern "C" int svg_debug_jit_check(const svg_problem* p, const int64_t* opts, in
     if (opts) {
       e.opt_tile = opts[0];
       e.opt_reg_bits = opts[1];
-      e.opt_reg_bits_fwd = opts[2];
-      e.opt_acc_kb = opts[3];
     }
     (void)lower(&e, p, true);
     (void)cudaGetLastError();

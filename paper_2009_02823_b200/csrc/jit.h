@@ -30,12 +30,7 @@ struct JitPass {
   int nslots = 0;
   bool thread_acc = false, tiles = false;
   int acc_shift = 0;                 // thread_acc: lanes combined per accumulator (log2)
-  bool fuse_diag = true;             // reverse passes: fuse runs of diagonal rotations
-  bool acc_prefetch = true;          // reverse passes: load an op's accumulator before the op
   bool scale_carry = false;          // deferred scale carried across layout changes (no shared-memory segments)
-  bool early_stage = false;          // reverse passes: next tile's phi staged at tile start (see jit.cu)
-  bool stage = true;                 // stage the next tile with cp.async (passes without transposes)
-  int min_blocks = 0;                // __launch_bounds__ min blocks per SM (0: default)
   uint64_t rest = 0;
   const uint8_t* q = nullptr;        // tile qubits (PassDesc.q)
   const uint8_t* swz = nullptr;      // shared-memory swizzle columns per tile position (engine.cu Swizzle)

@@ -49,31 +49,21 @@ def test_gpu_matches_reference_golden_large(name):
     assert vars(rep.counters) == gold["counters"]
 
 
-_VARIANTS = {  # generated-kernel plan options (engine defaults: all on / auto)
+_VARIANTS = {  # generated-kernel plan options (engine defaults: auto)
     "wide_tiles": {"tile_qubits": 12, "tile_fwd": -1},
-    "wide_tiles_fixed_lanes": {"tile_qubits": 12, "free_lanes": 0},
     "fwd_split_13": {"tile_qubits": 12, "tile_fwd": 13},
     "fwd_split_12": {"tile_qubits": 11, "tile_fwd": 12},
-    "no_scale_carry": {"scale_carry": 0},
-    "no_fused_diag": {"fuse_diag": 0},
-    "no_acc_prefetch_acc8": {"acc_prefetch": 0, "acc_kb": 8},
-    "lane_cost_low": {"lane_cost10": 10},
-    "direct_store": {"direct_store": 1},
-    "direct_store_wide": {"direct_store": 1, "tile_qubits": 12},
-    "no_early_fwd": {"early_fwd": 0},
-    "early_stage": {"early_stage": 1},
-    "early_stage_wide": {"early_stage": 1, "tile_qubits": 12},
-    "early_stage_fixed_lanes": {"early_stage": 1, "free_lanes": 0},
-    "no_pdl_no_stage": {"pdl": 0, "stage": 0},
+    "low_qubits_5": {"low_qubits": 5},
+    "low_qubits_4_wide": {"low_qubits": 4, "tile_qubits": 12},
+    "reg_bits_3": {"reg_bits": 3},
 }
 
 
 @pytest.mark.parametrize("variant", sorted(_VARIANTS))
 @pytest.mark.parametrize("name", ["cfg3_n20", "cfg5_n20"])
 def test_generated_kernel_variants_match_reference_golden(name, variant):
-    """Every plan / code-generation option of the generated kernels (free-lane
-    layouts, swizzled transposes, 12-qubit tiles, separate forward schedules,
-    carried scales, fused diagonal runs, accumulator modes) against the golden."""
+    """Every plan option of the generated kernels (tile widths, separate forward
+    schedules, forced low qubits, register bits) against the golden."""
     gold = load_golden(f"golden_{name}.json")[name]
     circ, theta, obs, inp, method = materialize(large_config_cases()[name])
     opts = {"jit": 2, **_VARIANTS[variant]}
@@ -83,9 +73,7 @@ def test_generated_kernel_variants_match_reference_golden(name, variant):
             eng.set_option(k, v)
         rep = _run(circ, theta, obs, inp, method)
     finally:
-        for k, v in {"jit": 1, "tile_qubits": 0, "tile_fwd": 0, "free_lanes": 1, "scale_carry": 1, "fuse_diag": 1,
-                     "acc_prefetch": 1, "acc_kb": 0, "lane_cost10": 37, "direct_store": 0, "early_fwd": 1, "early_stage": 0,
-                     "pdl": 1, "stage": 1}.items():
+        for k, v in {"jit": 1, "tile_qubits": 0, "tile_fwd": 0, "low_qubits": 3, "reg_bits": 0}.items():
             eng.set_option(k, v)
     assert max_err(rep.values, cvec(gold["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*gold["energy"])) <= ENERGY_TOL
@@ -123,7 +111,7 @@ def test_both_kernel_families_match_golden(name, kernel, reg_bits):
     """Shared-memory tiles (1) and interpreted register tiles (2, R = 3 / 4) against the reference's outputs."""
     rec = GOLD[name]
     circ, theta, obs, inp, _ = materialize(SMALL[name])
-    rep = _with_options({"kernel": kernel, "reg_bits": reg_bits, "reg_bits_fwd": reg_bits},
+    rep = _with_options({"kernel": kernel, "reg_bits": reg_bits},
                         lambda: sv.reverse_mode_gradient(circ, theta, obs, inp))
     assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
@@ -308,7 +296,7 @@ def test_circuit_specialised_kernels_match_golden(name, reg_bits):
     stats = {}
     run = (lambda: sv.non_hermitian_gradient(circ, theta, obs, inp)) if method == "non_hermitian" else \
         (lambda: sv.reverse_mode_gradient(circ, theta, obs, inp, stats=stats))
-    rep = _with_options({"jit": 2, "reg_bits": reg_bits, "reg_bits_fwd": reg_bits, "tile_qubits": 9}, run)
+    rep = _with_options({"jit": 2, "reg_bits": reg_bits, "tile_qubits": 9}, run)
     sv._native.engine().set_option("jit", 1)
     assert max_err(rep.values, cvec(rec["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*rec["energy"])) <= ENERGY_TOL
