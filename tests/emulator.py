@@ -112,8 +112,15 @@ def _product_terms(prob, psi, l2p=None, nloc=None, rank=0, fetch=None):
 def emulate(circuit, params, obs, input_state, tile_qubits=0, sms=0):
     """(sums complex[P], energy, pass_count) computed from the lowered tables."""
     prob = Problem(circuit, np.asarray(params, dtype=float), obs, input_state)
-    n = circuit.num_qubits
     order, start, qmasks, k = _native.plan_inspect(prob.c, tile_qubits, sms)
+    sums, energy = emulate_order(circuit, params, obs, input_state, order)
+    return sums, energy, (order, start, qmasks, k)
+
+
+def emulate_order(circuit, params, obs, input_state, order):
+    """(sums complex[P], energy) of the adjoint sweep with the gates applied in
+    `order` (forward) and its reverse (the engine's schedule, dense numpy)."""
+    prob = Problem(circuit, np.asarray(params, dtype=float), obs, input_state)
     gates, derivs, terms = prob.gates, prob.derivs, prob.terms
     psi = np.array(input_state.amplitudes, dtype=complex)
     for gi in order:
@@ -125,26 +132,25 @@ def emulate(circuit, params, obs, input_state, tile_qubits=0, sms=0):
     energy = np.vdot(psi, lam)
     first = np.concatenate([[0], np.cumsum(gates["nderiv"])]).astype(int)
     contrib = np.zeros(len(derivs), dtype=complex)
-    for p in range(len(start) - 2, -1, -1):
-        for gi in order[start[p]: start[p + 1]][::-1]:
-            g = gates[gi]
-            for j in range(int(g["nderiv"])):  # generators in the post-gate basis see phi_{i+1}
-                d = first[gi] + j
-                if derivs[d]["basis"] == 1:
-                    contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
-            psi = _apply(psi, g, "rewind")
-            for j in range(int(g["nderiv"])):
-                d = first[gi] + j
-                if derivs[d]["basis"] == 0:
-                    contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
-            if gi > 0:
-                lam = _apply(lam, g, "adjoint")
+    for gi in list(order)[::-1]:
+        g = gates[gi]
+        for j in range(int(g["nderiv"])):  # generators in the post-gate basis see phi_{i+1}
+            d = first[gi] + j
+            if derivs[d]["basis"] == 1:
+                contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
+        psi = _apply(psi, g, "rewind")
+        for j in range(int(g["nderiv"])):
+            d = first[gi] + j
+            if derivs[d]["basis"] == 0:
+                contrib[d] = np.vdot(lam, _generator(psi, g, derivs[d]["k"]))
+        if gi > 0:
+            lam = _apply(lam, g, "adjoint")
     sums = np.zeros(circuit.num_params, dtype=complex)
     for gi in range(len(gates) - 1, -1, -1):
         for j in range(int(gates[gi]["nderiv"])):
             d = first[gi] + j
             sums[derivs[d]["param_ref"]] += contrib[d]
-    return sums, complex(energy), (order, start, qmasks, k)
+    return sums, complex(energy)
 
 
 # ---- sharded schedule (one rank's view) -------------------------------------------
