@@ -502,10 +502,6 @@ constexpr int kRegPassGates = 40;
 // States this large (per shard) stream HBM: generated kernels use 12-qubit tiles
 // (a narrower reverse tile gets a forward schedule over k+1-qubit tiles).
 constexpr int kWideTileQubits = 24;
-// Chunk groups (HBM-resident single-shard states): a CTA owns a chunk of
-// 2^(k + kChunkExtra) amplitudes per buffer (L2-resident while the group's passes
-// run over it: 148 CTAs x 2 buffers x 256 KB = 74 MB at k = 12).
-constexpr int kChunkExtra = 2;
 // Segment-plan cost model in register-op units (a register rotation = 1): a lane
 // flip is a warp shuffle of both buffers (forward: one), a layout change a
 // shared-memory transpose.  Measured with tools/pass_model.py (round 1).
@@ -817,8 +813,15 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     pp.max_items = kRegPassGates;
   // chunk groups: generated kernels, one shard, HBM-resident state
   if (jit_planned && g == 0 && e->shards_local == 1 && e->opt_chunk >= 0) {
-    const int c = e->opt_chunk > 0 ? static_cast<int>(e->opt_chunk) : (nloc >= kWideTileQubits ? L.k + kChunkExtra : 0);
+    // auto: off for HBM-resident states -- measured slower (cfg 4: 0.56 vs 0.71
+    // gradients/s at k + 2, cfg 3: 6.3 vs 8.4; the members' per-tile memory phases
+    // (staging, transposes, stores) are SM-side costs an L2-resident chunk does not
+    // shorten, and members carry fewer gates than plain passes)
+    const int c = e->opt_chunk > 0 ? static_cast<int>(e->opt_chunk) : 0;
     if (c > L.k && c < nloc) pp.chunk = c;
+    // a state that is one tile: the passes of each sweep run as whole-state groups
+    // (one kernel and one CTA for several passes)
+    if (nloc <= L.k) pp.chunk = nloc;
   }
   const int64_t S = int64_t(16) << nloc;  // bytes of one state shard
 

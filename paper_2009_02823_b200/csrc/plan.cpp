@@ -132,6 +132,32 @@ std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, in
                                 std::vector<int>* l2p_final) {
   const int nloc = n - g;
   if (pp.n != nloc) throw std::runtime_error("plan_schedule: PlanParams.n must be the local qubit count");
+  if (g == 0 && pp.chunk >= nloc && nloc <= pp.k) {
+    // the whole state is one tile: consecutive passes form groups (one kernel, one
+    // CTA, no launch between passes) while their derivative slots fit the
+    // accumulators
+    PlanParams pq = pp;
+    pq.chunk = 0;
+    std::vector<Step> steps = plan_schedule(logical, n, g, pq, l2p_final);
+    int gid = 0, derivs = 0;
+    for (size_t j = 0; j < steps.size(); ++j) {
+      int d = 0;
+      for (int gi : steps[j].pass.items) d += logical[gi].nderiv;
+      if (j > 0 && derivs + d > pp.max_group_derivs) {
+        ++gid;
+        derivs = 0;
+      }
+      derivs += d;
+      steps[j].group = gid;
+      steps[j].chunk = low_mask(nloc);
+    }
+    for (size_t j = 0; j < steps.size(); ++j) {  // single-pass groups are plain passes
+      const bool alone = (j == 0 || steps[j - 1].group != steps[j].group) &&
+                         (j + 1 == steps.size() || steps[j + 1].group != steps[j].group);
+      if (alone) steps[j].group = -1, steps[j].chunk = 0;
+    }
+    return steps;
+  }
   if (pp.chunk > pp.k && pp.chunk < nloc) {
     if (g != 0) throw std::runtime_error("chunked schedules are for single-shard states");
     if (l2p_final) {
