@@ -192,9 +192,7 @@ int svg_engine_create_sharded(int device, int world, int rank, const uint8_t ncc
 int svg_engine_destroy(svg_engine* e);
 /* Launch on an external cudaStream_t (passed as void*); NULL = engine's own stream. */
 int svg_engine_set_stream(svg_engine* e, void* stream);
-/* Options (10): "tile_qubits" (0 = auto), "tile_fwd" (forward-only tile qubits, 0 auto, -1 off),
-   "chunk_qubits" (chunk groups of HBM-resident states: several passes per kernel over
-   L2-resident chunks of 2^chunk amplitudes; 0 auto, -1 off),
+/* Options (9): "tile_qubits" (0 = auto), "tile_fwd" (forward-only tile qubits, 0 auto, -1 off),
    "low_qubits" (3..5: contiguous low qubits every generated-kernel tile holds), "reg_bits"
    (0 auto, 3 or 4: 2^bits amplitudes per thread per buffer), "max_gates_per_pass" (0 = auto),
    "kernel" (0 auto, 1 shared-memory tiles, 2 register tiles), "jit" (circuit-specialised

@@ -145,13 +145,6 @@ struct Launch {
   bool tiles = false;  // L_REG: stages the tile through shared memory
   int gbit = 0, lpos = 0;  // L_SWAP: rank bit <-> local position
   std::shared_ptr<JitKernel> jit;  // L_REG: circuit-specialised kernel (jit.cu), or null: interpreter
-  // chunk groups (jit.h JitGroup): consecutive L_REG launches of one group run as
-  // ONE generated kernel, launched at the head; the others only describe members
-  int group = -1;        // group id (-1: a pass of its own)
-  uint64_t chunk = 0;    // the group's chunk qubits (local positions)
-  int head = -1;         // index of the group's head launch in its list (own index for a head)
-  int slot_off = 0;      // first accumulator slot of this member in the group kernel
-  int gslots = 0;        // head: slots of the whole group
   Swizzle swz;                     // L_REG: shared-memory swizzle of the pass's transposes
   // L_PROD: this pass's factors; first pass reads psi (or the partner shard), later
   // ones the product buffer; the last one's scalar per source shard is
@@ -202,9 +195,6 @@ struct svg_engine {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 0;  // reg bits 0: auto
-  // chunk groups for HBM-resident single-shard states (generated kernels): chunk
-  // qubits, 0 auto (tile + kChunkExtra), -1 off
-  int64_t opt_chunk = 0;
   // virtual engines: run the NCCL-mode data path (half-shard pack -> copy ->
   // unpack, partner fetch into scratch) with device copies as the transport
   int64_t opt_emulate_transport = 0;
@@ -212,7 +202,7 @@ struct svg_engine {
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
-  int64_t opt_low_qubits = 3;    // generated kernels: contiguous low qubits every tile holds (3..5)
+  int64_t opt_low_qubits = 4;    // generated kernels: contiguous low qubits every tile holds (3..5)
   mutable std::string jit_error;
   bool jit_dry_run = false;        // svg_debug_jit_check
   mutable int jit_dry_count = 0;
@@ -692,68 +682,6 @@ thread_local std::chrono::steady_clock::time_point g_phase_t;
 // fwd_ready (optional): called once the forward launches are complete and sized
 // -- generated kernels only, no shared-memory segments -- so the caller can start
 // them while the rest (observable, reverse sweep) is still being lowered.
-// Chunk groups of a launch list: a launch continuing its predecessor's group is a
-// member of the predecessor's head; returns the member count (launches that are
-// not heads).
-int assign_heads(std::vector<Launch>& v) {
-  int members = 0;
-  for (size_t i = 0; i < v.size(); ++i) {
-    Launch& l = v[i];
-    if (l.kind == L_REG && l.group >= 0 && i > 0 && v[i - 1].kind == L_REG && v[i - 1].group == l.group) {
-      l.head = v[i - 1].head;
-      l.slot_off = v[i - 1].slot_off + v[i - 1].d.nslots;
-      ++members;
-    } else {
-      l.head = static_cast<int>(i);
-      l.slot_off = 0;
-    }
-    v[l.head].gslots = l.slot_off + l.d.nslots;
-  }
-  return members;
-}
-
-// Generator input of one register-tile launch.
-JitPass jit_pass_of(const Lowered& L, const Launch& l, int nloc, bool carry) {
-  JitPass jp;
-  jp.R = l.R;
-  jp.nb = l.nb;
-  jp.k = l.d.k;
-  jp.nloc = nloc;
-  jp.threads = l.threads;
-  jp.nslots = l.d.nslots;
-  jp.thread_acc = l.d.thread_acc != 0;
-  jp.acc_shift = l.d.acc_shift;
-  jp.tiles = l.tiles;
-  jp.rest = l.d.rest;
-  jp.q = l.d.q;
-  jp.swz = l.swz.col;
-  jp.scale_carry = carry;
-  jp.segs = L.segs.data() + l.d.seg_begin;
-  jp.nsegs = l.d.seg_end - l.d.seg_begin;
-  jp.rops = L.rops.data() + l.d.op_begin;
-  jp.op_begin = l.d.op_begin;
-  return jp;
-}
-
-// The generated kernel of head launch h (itself and its group members).
-JitGroup jit_group_of(const Lowered& L, const std::vector<Launch>& v, size_t h, int nloc, bool carry) {
-  JitGroup g;
-  for (size_t i = h; i < v.size() && v[i].head == static_cast<int>(h); ++i) g.members.push_back(jit_pass_of(L, v[i], nloc, carry));
-  g.chunk = g.members.size() > 1 ? v[h].chunk : 0;
-  return g;
-}
-
-// Launch parameters of head launch h's generated kernel.
-std::vector<unsigned char> group_args(const Lowered& L, const std::vector<Launch>& v, size_t h, const JitArgsHead& head) {
-  std::vector<const SegDesc*> segs;
-  std::vector<const RegOp*> rops;
-  for (size_t i = h; i < v.size() && v[i].head == static_cast<int>(h); ++i) {
-    segs.push_back(L.segs.data() + v[i].d.seg_begin);
-    rops.push_back(L.rops.data() + v[i].d.op_begin);
-  }
-  return jit_args(*v[h].jit, head, segs, rops);
-}
-
 Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
               const std::function<void(Lowered&)>& fwd_ready = {}, bool interp_only = false) {
   g_phase_t = std::chrono::steady_clock::now();
@@ -800,8 +728,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
                            (e->jit_dry_run || jit_available(nullptr));
   L.jit_planned = jit_planned;
   // Generated kernels address the global tile through the lanes' physical qubits, so
-  // their tiles need only qubits 0..low_qubits-1 (128-byte rows at 3) instead of
-  // 0..4: more tile qubits free for the circuit (cfg 4: 61 -> 52 passes per sweep)
+  // their tiles need only qubits 0..low_qubits-1 (256-byte rows at 4) instead of
+  // 0..4: more tile qubits free for the circuit.  cfg 4: 61 / 56 / 52 passes per
+  // sweep at 5 / 4 / 3 low qubits, measured 0.708 / 0.758 / 0.714 gradients/s (at 3
+  // the 128-byte rows cost more per pass than the 4 saved passes)
   if (jit_planned && nloc > L.k && e->opt_low_qubits < L.b) L.b = static_cast<int>(e->opt_low_qubits);
   PlanParams pp;
   pp.n = nloc;
@@ -811,18 +741,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     pp.max_items = static_cast<int>(e->opt_max_items);
   else if (L.reg)
     pp.max_items = kRegPassGates;
-  // chunk groups: generated kernels, one shard, HBM-resident state
-  if (jit_planned && g == 0 && e->shards_local == 1 && e->opt_chunk >= 0) {
-    // auto: off for HBM-resident states -- measured slower (cfg 4: 0.56 vs 0.71
-    // gradients/s at k + 2, cfg 3: 6.3 vs 8.4; the members' per-tile memory phases
-    // (staging, transposes, stores) are SM-side costs an L2-resident chunk does not
-    // shorten, and members carry fewer gates than plain passes)
-    const int c = e->opt_chunk > 0 ? static_cast<int>(e->opt_chunk) : 0;
-    if (c > L.k && c < nloc) pp.chunk = c;
-    // a state that is one tile: the passes of each sweep run as whole-state groups
-    // (one kernel and one CTA for several passes)
-    if (nloc <= L.k) pp.chunk = nloc;
-  }
   const int64_t S = int64_t(16) << nloc;  // bytes of one state shard
 
   std::vector<GateShape> logical(p->num_gates);
@@ -831,8 +749,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // the schedule is a pure function of the gate shapes and plan parameters: memoised
   auto schedule = [&](const PlanParams& pq, std::vector<int>* l2p_out) {
     Hasher h;
-    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs, pq.chunk, pq.max_group_derivs,
-                            static_cast<int32_t>(logical.size())};
+    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs, static_cast<int32_t>(logical.size())};
     h.pod(head);
     for (const GateShape& sh : logical) {
       h.word(sh.flip);
@@ -1068,14 +985,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       l.d.seg_end = static_cast<int>(L.segs.size());
       l.d.op_end = static_cast<int>(L.rops.size());
       if (psegs_f[si]->size() > 1) l.tiles = true;
-      l.group = fsteps[si].group;
-      l.chunk = fsteps[si].chunk;
       L.fwd.push_back(l);
     }
     L.pass_bytes += 2 * S;
   }
-
-  L.pass_bytes -= int64_t(assign_heads(L.fwd)) * 2 * S;  // a chunk group streams HBM once
 
   // Early forward launches: generated kernels with register segments only need
   // no device tables (their coefficients travel in the launch parameters).
@@ -1086,22 +999,34 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       for (int si = l.d.seg_begin; ok && si < l.d.seg_end; ++si) ok = L.segs[si].kind == SEG_REG;
     }
     if (ok) {
-      std::vector<JitGroup> groups;
-      std::vector<size_t> heads;
-      for (size_t i = 0; i < L.fwd.size(); ++i)
-        if (L.fwd[i].head == static_cast<int>(i)) {
-          groups.push_back(jit_group_of(L, L.fwd, i, nloc, carry));
-          heads.push_back(i);
-        }
+      std::vector<JitPass> passes;
+      for (Launch& l : L.fwd) {
+        JitPass jp;
+        jp.R = l.R;
+        jp.nb = 1;
+        jp.k = l.d.k;
+        jp.nloc = nloc;
+        jp.threads = l.threads;
+        jp.tiles = l.tiles;
+        jp.rest = l.d.rest;
+        jp.q = l.d.q;
+        jp.swz = l.swz.col;
+        jp.scale_carry = carry;
+        jp.segs = L.segs.data() + l.d.seg_begin;
+        jp.nsegs = l.d.seg_end - l.d.seg_begin;
+        jp.rops = L.rops.data() + l.d.op_begin;
+        jp.op_begin = l.d.op_begin;
+        passes.push_back(jp);
+      }
       std::vector<std::shared_ptr<JitKernel>> ks;
       try {
-        ks = jit_get(groups, e->device);
+        ks = jit_get(passes, e->device);
       } catch (const std::exception& ex) {
         throw JitFailure(ex.what());
       }
-      for (size_t gi = 0; gi < ks.size(); ++gi) {
-        Launch& l = L.fwd[heads[gi]];
-        l.jit = ks[gi];
+      for (size_t i = 0; i < ks.size(); ++i) {
+        Launch& l = L.fwd[i];
+        l.jit = ks[i];
         l.smem = l.jit->smem;
         if (l.jit->blocks_per_sm <= 0) {
           int blocks = 0;
@@ -1112,7 +1037,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
           }
           l.jit->blocks_per_sm = blocks;
         }
-        const int64_t nt = int64_t(1) << (nloc - (groups[gi].chunk ? __builtin_popcountll(groups[gi].chunk) : l.d.k));
+        const int64_t nt = int64_t(1) << (nloc - l.d.k);
         l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nt, int64_t(e->sms) * l.jit->blocks_per_sm)));
       }
       fwd_ready(L);
@@ -1382,20 +1307,15 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         l.d.op_end = static_cast<int>(L.rops.size());
         if (sgs.size() > 1) l.tiles = true;
         l.d.nslots = static_cast<int>(slot);
-        l.group = steps[si].group;
-        l.chunk = steps[si].chunk;
         L.rev.push_back(l);
       }
       L.pass_bytes += 4 * S;
     }
   }
 
-  L.pass_bytes -= int64_t(assign_heads(L.rev)) * 4 * S;
-
   SVGB_PHASE(6);
   // grids, shared memory, partial offsets
-  auto ntiles_of = [&](const Launch& l) {  // work items of a launch: tiles, or chunks of a group kernel
-    if (l.kind == L_REG && l.chunk) return int64_t(1) << (nloc - __builtin_popcountll(l.chunk));
+  auto ntiles_of = [&](const Launch& l) {
     return int64_t(1) << (nloc - ((l.kind == L_REG || l.kind == L_OBS) ? l.d.k : L.k));
   };
   // lane-group inner-product accumulators: combine 2^shift lanes so that the
@@ -1489,37 +1409,47 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // circuit-specialised kernels for the register-tile passes
   const bool want_jit = L.reg && (e->opt_jit == 2 || (e->opt_jit == 1 && nloc >= kJitMinQubits));
   if (want_jit) {
-    std::vector<Launch*> regl;  // head launches still without a kernel
-    std::vector<JitGroup> passes;
+    std::vector<Launch*> regl;
     for (std::vector<Launch>* v : {&L.fwd, &L.rev})
-      for (size_t h = 0; h < v->size(); ++h) {
-        Launch& l = (*v)[h];
-        if (l.kind != L_REG || l.jit || l.head != static_cast<int>(h)) continue;
-        size_t end = h + 1;
-        while (end < v->size() && (*v)[end].head == static_cast<int>(h)) ++end;
-        // accumulator mode of the kernel (all members share it): per-thread
-        // accumulators when the group has slots, lanes combined in groups of
-        // 2^shift until they fit.  Auto budget: the SM's shared memory split over
-        // the kernel's CTAs per SM, minus the tile / staging buffers and the
-        // per-warp accumulators.  Every halving of the accumulators costs a
-        // butterfly step per op (measured: 40-slot passes 8 % slower at shift 1).
-        const int nsl = l.gslots;
-        const bool tacc = l.nb == 2 && nsl > 0;
-        int shift = 0;
-        if (tacc) {
-          const int blocks = l.nb == 2 ? std::max(1, std::min(2, 256 / l.threads)) : (l.R == 3 ? 2 : 4);
-          const size_t share = std::min<size_t>(e->max_smem, (size_t(e->max_smem_sm) / blocks) - 1024);
-          const size_t fixed = (sizeof(double2) << l.d.k) * l.nb + sizeof(double2) * (l.threads / 32) * nsl;
-          const size_t budget = share > fixed + 4096 ? share - fixed : 4096;
-          while (shift < 5 && size_t(nsl) * (l.threads >> shift) * sizeof(double) > budget) ++shift;
-        }
-        for (size_t i = h; i < end; ++i) {
-          (*v)[i].d.thread_acc = tacc;
-          (*v)[i].d.acc_shift = shift;
-        }
-        passes.push_back(jit_group_of(L, *v, h, nloc, carry));
-        regl.push_back(&l);
+      for (Launch& l : *v)
+        if (l.kind == L_REG && !l.jit) regl.push_back(&l);
+    std::vector<JitPass> passes;
+    passes.reserve(regl.size());
+    for (Launch* l : regl) {
+      set_thread_acc(*l);
+      if (l->d.thread_acc) {
+        // auto budget: the SM's shared memory split over the kernel's CTAs per SM,
+        // minus tile / staging buffers and per-warp accumulators.  Every halving
+        // of the accumulators costs a butterfly step per op (measured: 40-slot
+        // passes 8 % slower at shift 1 than at shift 0).
+        const int blocks = l->nb == 2 ? std::max(1, std::min(2, 256 / l->threads)) : (l->R == 3 ? 2 : 4);
+        const size_t share = std::min<size_t>(e->max_smem, (size_t(e->max_smem_sm) / blocks) - 1024);
+        const size_t fixed = (sizeof(double2) << l->d.k) * l->nb + sizeof(double2) * (l->threads / 32) * l->d.nslots;
+        const size_t budget = share > fixed + 4096 ? share - fixed : 4096;
+        l->d.acc_shift = 0;
+        while (l->d.acc_shift < 5 && size_t(l->d.nslots) * (l->threads >> l->d.acc_shift) * sizeof(double) > budget)
+          ++l->d.acc_shift;
       }
+      JitPass jp;
+      jp.R = l->R;
+      jp.nb = l->nb;
+      jp.k = l->d.k;
+      jp.nloc = nloc;
+      jp.threads = l->threads;
+      jp.nslots = l->d.nslots;
+      jp.thread_acc = l->d.thread_acc != 0;
+      jp.acc_shift = l->d.acc_shift;
+      jp.tiles = l->tiles;
+      jp.rest = l->d.rest;
+      jp.q = l->d.q;
+      jp.swz = l->swz.col;
+      jp.scale_carry = carry;
+      jp.segs = L.segs.data() + l->d.seg_begin;
+      jp.nsegs = l->d.seg_end - l->d.seg_begin;
+      jp.rops = L.rops.data() + l->d.op_begin;
+      jp.op_begin = l->d.op_begin;
+      passes.push_back(jp);
+    }
     try {
       std::string why;
       if (!jit_available(&why)) throw std::runtime_error(why);
@@ -1558,19 +1488,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       e->jit_error = ex.what();  // auto: keep the interpreted kernels
     }
   }
-  // group members launch with their head (same grid, partials in the head's block)
-  auto size_list = [&](std::vector<Launch>& v) {
-    for (size_t i = 0; i < v.size(); ++i) {
-      Launch& l = v[i];
-      if (l.kind == L_REG && l.head != static_cast<int>(i)) {
-        l.grid = v[l.head].grid;
-        l.smem = 0;
-        continue;
-      }
-      size_launch(l);
-    }
-  };
-  size_list(L.fwd);
+  for (Launch& l : L.fwd) size_launch(l);
   for (Launch& l : L.obs) {
     size_launch(l);
     if (l.kind == L_FETCH) continue;
@@ -1578,23 +1496,18 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     part += l.grid;
   }
   const int64_t energy_count = part - energy_off;
-  size_list(L.rev);
-  for (size_t i = 0; i < L.rev.size(); ++i) {
-    Launch& l = L.rev[i];
+  for (Launch& l : L.rev) {
+    size_launch(l);
     if (l.kind == L_SWAP) continue;
-    if (l.kind == L_REG && l.head != static_cast<int>(i)) {
-      l.d.part_off = L.rev[l.head].d.part_off;
-      continue;
-    }
     l.d.part_off = part;
-    part += int64_t(l.kind == L_REG ? l.gslots : l.d.nslots) * l.grid;
+    part += int64_t(l.d.nslots) * l.grid;
   }
   L.partial_count = part;
   if (with_reverse) {
     L.sums.resize(p->num_derivs + 1);
     for (int d = 0; d < p->num_derivs; ++d) {
       const Launch& l = L.rev[deriv_slot[d].first];
-      L.sums[d] = SumSpec{l.d.part_off + int64_t(l.slot_off + deriv_slot[d].second) * l.grid, l.grid};
+      L.sums[d] = SumSpec{l.d.part_off + int64_t(deriv_slot[d].second) * l.grid, l.grid};
     }
   } else {
     L.sums.resize(1);
@@ -1683,11 +1596,10 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       CK(cudaEventRecord(e->ev[1], e->stream));
       fwd_cb = [&](Lowered& Lf) {
         double2* psi0 = static_cast<double2*>(e->psi.ptr);
-        for (size_t i = 0; i < Lf.fwd.size(); ++i) {
-          const Launch& l = Lf.fwd[i];
-          if (l.head != static_cast<int>(i)) continue;  // chunk-group member: runs inside its head's kernel
+        for (const Launch& l : Lf.fwd) {
           const JitArgsHead head{psi0, nullptr, nullptr, nullptr, nullptr, l.d.part_off, 0};
-          std::vector<unsigned char> args = group_args(Lf, Lf.fwd, i, head);
+          std::vector<unsigned char> args =
+              jit_args(*l.jit, head, Lf.segs.data() + l.d.seg_begin, Lf.rops.data() + l.d.op_begin);
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3(l.grid);
           cfg.blockDim = dim3(l.threads);
@@ -1832,20 +1744,16 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), params));
     };
     // register-tile pass: the circuit-specialised kernel when there is one, else the interpreter
-    // (v[i] of launch list v; a chunk-group member launches nothing: its head's kernel runs it)
-    auto launch_reg = [&](const std::vector<Launch>& v, size_t i, const PassDesc& d, double2* b0, double2* b1,
-                          double2* prt) {
-      const Launch& l = v[i];
-      if (l.head != static_cast<int>(i)) return false;
+    auto launch_reg = [&](const Launch& l, const PassDesc& d, double2* b0, double2* b1, double2* prt) {
       if (!l.jit) {
         launch_pass_reg(l.nb, l.R, d, l.grid, l.threads, l.smem, s, b0, b1, dsegs, drops, dops, dcoef, prt);
-        return true;
+        return;
       }
       const JitArgsHead head{b0, b1, dops, dcoef, prt, d.part_off, d.rank_bits};
-      std::vector<unsigned char> args = group_args(L, v, i, head);
+      std::vector<unsigned char> args =
+          jit_args(*l.jit, head, L.segs.data() + d.seg_begin, L.rops.data() + d.op_begin);
       launch_generated(l.jit->fn, l.grid, l.threads, l.smem, s, args);
       ++jit_launches;
-      return true;
     };
     int64_t launches = 0, h2d = bl.total, d2h = 0;
     const auto t_launch = std::chrono::steady_clock::now();
@@ -1870,8 +1778,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     }
     launches += early_launches;
     if (!init_done) CK(cudaEventRecord(e->ev[1], s));
-    for (size_t i = 0; i < L.fwd.size(); ++i) {
-      const Launch& l = L.fwd[i];
+    for (const Launch& l : L.fwd) {
       if (L.fwd_early) break;  // launched by the fwd_ready callback
       if (l.kind == L_SWAP) {
         swap_buffer(psi, l.gbit, l.lpos);
@@ -1881,12 +1788,11 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         const ShardView v = view(sh);
         PassDesc d = l.d;
         d.rank_bits = v.rank_bits;
-        if (l.kind == L_REG) {
-          launches += launch_reg(L.fwd, i, d, v.psi, nullptr, v.part);
-        } else {
+        if (l.kind == L_REG)
+          launch_reg(l, d, v.psi, nullptr, v.part);
+        else
           launch_fwd(d, l.grid, l.smem, s, v.psi, dops, dcoef);
-          ++launches;
-        }
+        ++launches;
       }
     }
     if (!L.fwd_early) CK(cudaEventRecord(e->ev[2], s));
@@ -1937,8 +1843,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       }
     }
     CK(cudaEventRecord(e->ev[3], s));
-    for (size_t i = 0; i < L.rev.size(); ++i) {
-      const Launch& l = L.rev[i];
+    for (const Launch& l : L.rev) {
       if (l.kind == L_SWAP) {
         swap_buffer(psi, l.gbit, l.lpos);
         swap_buffer(lam, l.gbit, l.lpos);
@@ -1948,12 +1853,11 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         const ShardView v = view(sh);
         PassDesc d = l.d;
         d.rank_bits = v.rank_bits;
-        if (l.kind == L_REG) {
-          launches += launch_reg(L.rev, i, d, v.psi, v.lam, v.part);
-        } else {
+        if (l.kind == L_REG)
+          launch_reg(l, d, v.psi, v.lam, v.part);
+        else
           launch_rev(d, l.grid, l.smem, s, v.psi, v.lam, dops, dcoef, v.part);
-          ++launches;
-        }
+        ++launches;
       }
     }
     CK(cudaEventRecord(e->ev[4], s));
@@ -2015,9 +1919,9 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       stats->ms_reverse = elapsed(e->ev[3], e->ev[4]);
       stats->ms_other = stats->ms_total - stats->ms_forward - stats->ms_observable - stats->ms_reverse;
       stats->launches = launches;
-      int fp = 0, rp = 0, op = 0;  // HBM passes: a chunk group's kernel counts once
-      for (size_t i = 0; i < L.fwd.size(); ++i) fp += L.fwd[i].kind != L_SWAP && L.fwd[i].head == static_cast<int>(i);
-      for (size_t i = 0; i < L.rev.size(); ++i) rp += L.rev[i].kind != L_SWAP && L.rev[i].head == static_cast<int>(i);
+      int fp = 0, rp = 0, op = 0;
+      for (const Launch& l : L.fwd) fp += l.kind != L_SWAP;
+      for (const Launch& l : L.rev) rp += l.kind != L_SWAP;
       for (const Launch& l : L.obs) op += l.kind != L_FETCH;
       stats->fwd_passes = fp;
       stats->obs_passes = op;
@@ -2213,9 +2117,6 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "tile_fwd") {
     if (value < -1 || value > 13) return fail(SVG_EINVAL, "tile_fwd must be in [-1, 13]");
     e->opt_tile_fwd = value;
-  } else if (k == "chunk_qubits") {
-    if (value < -1 || value > SVG_MAX_QUBITS) return fail(SVG_EINVAL, "chunk_qubits must be -1 (off), 0 (auto) or a qubit count");
-    e->opt_chunk = value;
   } else if (k == "low_qubits") {
     if (value < 3 || value > 5) return fail(SVG_EINVAL, "low_qubits must be in [3, 5]");
     e->opt_low_qubits = value;
@@ -2291,46 +2192,11 @@ extern "C" int svg_debug_jit_check(const svg_problem* p, const int64_t* opts, in
     if (opts) {
       e.opt_tile = opts[0];
       e.opt_reg_bits = opts[1];
-      e.opt_chunk = opts[2];
     }
     (void)lower(&e, p, true);
     (void)cudaGetLastError();
     if (npasses) *npasses = e.jit_dry_count;
     if (e.jit_error != "dry run") return fail(SVG_EINVAL, "generated kernels: " + e.jit_error);
-    return SVG_OK;
-  } catch (const std::exception& ex) {
-    return fail(SVG_EINVAL, ex.what());
-  }
-}
-
-// Debug (not in the public header): the chunk-group schedule of a single-shard
-// problem (plan_schedule with PlanParams.chunk), host only.  Per step j: gates
-// order[start[j] .. start[j+1]), tile qubits qmask[j], group id group[j] (-1: a
-// pass of its own) and the group's chunk qubits chunk[j].
-extern "C" int svg_debug_plan_chunked(const svg_problem* p, int tile_qubits, int low_qubits, int chunk,
-                                      int32_t* order_out, int32_t* start_out, uint64_t* qmask_out, int32_t* group_out,
-                                      uint64_t* chunk_out, int32_t* nsteps_out) {
-  try {
-    validate(p);
-    PlanParams pp;
-    pp.n = p->num_qubits;
-    pp.k = tile_qubits;
-    pp.b = low_qubits;
-    pp.max_items = kRegPassGates;
-    pp.chunk = chunk;
-    std::vector<GateShape> shapes(p->num_gates);
-    for (int i = 0; i < p->num_gates; ++i) shapes[i] = gate_shape(p->gates[i]);
-    const std::vector<Step> steps = plan_schedule(shapes, p->num_qubits, 0, pp, nullptr);
-    int pos = 0;
-    for (size_t j = 0; j < steps.size(); ++j) {
-      start_out[j] = pos;
-      qmask_out[j] = steps[j].pass.qmask;
-      group_out[j] = steps[j].group;
-      chunk_out[j] = steps[j].chunk;
-      for (int g : steps[j].pass.items) order_out[pos++] = g;
-    }
-    start_out[steps.size()] = pos;
-    *nsteps_out = static_cast<int32_t>(steps.size());
     return SVG_OK;
   } catch (const std::exception& ex) {
     return fail(SVG_EINVAL, ex.what());

@@ -40,19 +40,6 @@ struct JitPass {
   int op_begin = 0;
 };
 
-// A generated kernel: one pass (members.size() == 1, chunk == 0: every tile of the
-// state, grid-stride), or a group of passes run back to back over L2-resident
-// chunks.  A chunk is the set of 2^|chunk| amplitudes with fixed values of the
-// local positions outside `chunk`; every member's tile qubits lie inside it, so a
-// CTA takes a chunk, runs member 0 over its tiles, then member 1, ... (a CTA
-// barrier between members), and the chunk's amplitudes cross HBM once per group
-// instead of once per member.  Members share R, nb, k, threads and the
-// accumulator mode; their inner-product slots are numbered consecutively.
-struct JitGroup {
-  std::vector<JitPass> members;
-  uint64_t chunk = 0;  // local positions of the chunk qubits (0: single pass over the whole state)
-};
-
 // One tiled observable pass (k_obs_pass's work) for the generator.
 struct JitObsPass {
   int k = 0, b = 0, nloc = 0, threads = 256;
@@ -68,7 +55,6 @@ struct CoefRef {
   enum Kind : uint8_t { A, BB, KR, KAX, KAY, KBX, KBY, SCALE, TRE, TIM, KRRUN } kind;
   int index;    // register op (relative to op_begin) or segment (relative to seg_begin)
   int aux = 0;  // KRRUN: first op of the fused diagonal run (kr rescaled to the run's start)
-  int member = 0;  // group kernels: the member pass the op / segment belongs to
 };
 
 struct JitKernel {
@@ -76,7 +62,7 @@ struct JitKernel {
   int regs = 0;
   size_t smem = 0;                 // dynamic shared memory per CTA
   std::vector<CoefRef> coefs;      // fill order of the parameter block's c[]
-  std::vector<std::pair<int, int>> dop_segs;  // (member, segment): shared-memory segments whose DevOp base is a parameter
+  std::vector<int> dop_segs;       // shared-memory segments whose DevOp base is a parameter
   uint64_t device_mask = 0;        // devices whose kernel attributes are set
   int blocks_per_sm = 0;           // occupancy (same for every B200), 0 = not queried yet
 };
@@ -84,7 +70,7 @@ struct JitKernel {
 struct JitProgram {
   std::string src;
   std::vector<CoefRef> coefs;
-  std::vector<std::pair<int, int>> dop_segs;
+  std::vector<int> dop_segs;
   size_t smem = 0;
 };
 
@@ -113,14 +99,14 @@ struct JitObsArgsHead {
 bool jit_available(std::string* why);
 std::vector<std::shared_ptr<JitKernel>> jit_get_obs(const std::vector<JitObsPass>& passes, int device);
 std::vector<unsigned char> jit_obs_args(const JitKernel& kern, const JitObsArgsHead& head, const DevTerm* terms);
-JitProgram jit_generate(const JitGroup& g);
-// Kernels for the groups: cache hits by structural key; misses are generated
+JitProgram jit_generate(const JitPass& p);
+// Kernels for the passes: cache hits by structural key; misses are generated
 // and compiled (in parallel), then cached.  Throws std::runtime_error on compile / load failure.
 // device < 0: dry run -- generate and compile every distinct structure, load nothing, return {}.
-std::vector<std::shared_ptr<JitKernel>> jit_get(const std::vector<JitGroup>& groups, int device);
-// Parameter block for one launch: segs[m] / rops[m] are member m's segments and register ops.
-std::vector<unsigned char> jit_args(const JitKernel& kern, const JitArgsHead& head,
-                                    const std::vector<const SegDesc*>& segs, const std::vector<const RegOp*>& rops);
+std::vector<std::shared_ptr<JitKernel>> jit_get(const std::vector<JitPass>& passes, int device);
+// Parameter block for one launch.
+std::vector<unsigned char> jit_args(const JitKernel& kern, const JitArgsHead& head, const SegDesc* segs,
+                                    const RegOp* rops);
 size_t jit_cache_size();
 
 }  // namespace svgb

@@ -77,95 +77,10 @@ uint64_t remap_mask(uint64_t m, const std::vector<int>& l2p) {
   return r;
 }
 
-// Chunk groups (one shard): passes over pp.chunk-qubit tiles, each split into
-// k-qubit passes inside its chunk.  Inside a group the gates are planned in the
-// chunk's own coordinates (chunk qubits relabelled 0..c-1 in order, so the low
-// b qubits stay the low b; qubits outside the chunk -- only ever diagonal factors
-// or controls of the group's gates -- keep distinct positions above c).
-static std::vector<Step> plan_chunked(const std::vector<GateShape>& shapes, const PlanParams& pp) {
-  const int n = pp.n, c = pp.chunk;
-  PlanParams pc = pp;
-  pc.k = c;
-  pc.max_items = 1 << 30;
-  pc.max_derivs = pp.max_group_derivs;
-  const std::vector<Pass> sup = plan_gate_passes(shapes, pc);
-  std::vector<Step> steps;
-  std::vector<int> ident(n);
-  for (int q = 0; q < n; ++q) ident[q] = q;
-  int gid = 0;
-  for (const Pass& P : sup) {
-    int pos[64], inv[64];
-    int cc = 0, oc = 0;
-    for (int q = 0; q < n; ++q)
-      if ((P.qmask >> q) & 1) inv[cc] = q, pos[q] = cc++;
-    for (int q = 0; q < n; ++q)
-      if (!((P.qmask >> q) & 1)) pos[q] = c + oc++;
-    auto to_chunk = [&](uint64_t m) {
-      uint64_t r = 0;
-      for (uint64_t v = m; v; v &= v - 1) r |= 1ull << pos[__builtin_ctzll(v)];
-      return r;
-    };
-    std::vector<GateShape> sub(P.items.size());
-    for (size_t j = 0; j < P.items.size(); ++j) {
-      const GateShape& s0 = shapes[P.items[j]];
-      sub[j] = GateShape{to_chunk(s0.flip), to_chunk(s0.touch), s0.nderiv};
-    }
-    PlanParams ps = pp;
-    ps.n = c;
-    ps.chunk = 0;
-    const std::vector<Pass> members = plan_gate_passes(sub, ps);
-    for (const Pass& m : members) {
-      Step st;
-      for (int it : m.items) st.pass.items.push_back(P.items[it]);
-      for (uint64_t v = m.qmask; v; v &= v - 1) st.pass.qmask |= 1ull << inv[__builtin_ctzll(v)];
-      st.l2p = ident;
-      st.group = members.size() > 1 ? gid : -1;
-      st.chunk = members.size() > 1 ? P.qmask : 0;
-      steps.push_back(std::move(st));
-    }
-    ++gid;
-  }
-  return steps;
-}
-
 std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, int g, const PlanParams& pp,
                                 std::vector<int>* l2p_final) {
   const int nloc = n - g;
   if (pp.n != nloc) throw std::runtime_error("plan_schedule: PlanParams.n must be the local qubit count");
-  if (g == 0 && pp.chunk >= nloc && nloc <= pp.k) {
-    // the whole state is one tile: consecutive passes form groups (one kernel, one
-    // CTA, no launch between passes) while their derivative slots fit the
-    // accumulators
-    PlanParams pq = pp;
-    pq.chunk = 0;
-    std::vector<Step> steps = plan_schedule(logical, n, g, pq, l2p_final);
-    int gid = 0, derivs = 0;
-    for (size_t j = 0; j < steps.size(); ++j) {
-      int d = 0;
-      for (int gi : steps[j].pass.items) d += logical[gi].nderiv;
-      if (j > 0 && derivs + d > pp.max_group_derivs) {
-        ++gid;
-        derivs = 0;
-      }
-      derivs += d;
-      steps[j].group = gid;
-      steps[j].chunk = low_mask(nloc);
-    }
-    for (size_t j = 0; j < steps.size(); ++j) {  // single-pass groups are plain passes
-      const bool alone = (j == 0 || steps[j - 1].group != steps[j].group) &&
-                         (j + 1 == steps.size() || steps[j + 1].group != steps[j].group);
-      if (alone) steps[j].group = -1, steps[j].chunk = 0;
-    }
-    return steps;
-  }
-  if (pp.chunk > pp.k && pp.chunk < nloc) {
-    if (g != 0) throw std::runtime_error("chunked schedules are for single-shard states");
-    if (l2p_final) {
-      l2p_final->resize(n);
-      for (int q = 0; q < n; ++q) (*l2p_final)[q] = q;
-    }
-    return plan_chunked(logical, pp);
-  }
   const int G = static_cast<int>(logical.size());
   std::vector<int> l2p(n), p2l(n);
   for (int q = 0; q < n; ++q) l2p[q] = p2l[q] = q;

@@ -41,12 +41,6 @@ struct PlanParams {
   int b = 5;                 // forced contiguous low qubits
   int max_items = 256;       // gates per pass cap
   int max_derivs = 96;       // derivative slots per pass cap (shared-memory accumulators)
-  // Chunked schedules (one shard): passes are grouped into chunk groups of
-  // `chunk` qubits (> k); 0 = off.  A group's passes run in one kernel over
-  // L2-resident chunks (jit.h JitGroup); its derivative slots are capped by
-  // max_group_derivs (the group shares one accumulator array).
-  int chunk = 0;
-  int max_group_derivs = 96;
 };
 
 GateShape gate_shape(const svg_gate& g);
@@ -110,17 +104,12 @@ struct Step {
   int gbit = 0, lpos = 0;   // swap: rank bit gbit <-> local physical position lpos
   Pass pass;                // pass: items = gate indices, qmask over physical local positions
   std::vector<int> l2p;     // logical -> physical map in effect for this step's gates
-  int group = -1;           // chunked schedules: consecutive passes of one chunk group share an id
-  uint64_t chunk = 0;       // their chunk qubits (local positions), a superset of every member's tile
 };
 
 uint64_t remap_mask(uint64_t m, const std::vector<int>& l2p);
 
 // n total qubits, g rank bits (pp.n must be n - g); returns the forward schedule
 // and the final map (the observable and the reverse sweep start from it).
-// With pp.chunk > pp.k (one shard only) the passes come in chunk groups: the
-// gates are first planned into passes over pp.chunk-qubit "chunk tiles", and
-// each of those is planned again into k-qubit passes inside its chunk.
 std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, int g, const PlanParams& pp,
                                 std::vector<int>* l2p_final);
 

@@ -56,11 +56,7 @@ _VARIANTS = {  # generated-kernel plan options (engine defaults: auto)
     "low_qubits_5": {"low_qubits": 5},
     "low_qubits_4_wide": {"low_qubits": 4, "tile_qubits": 12},
     "reg_bits_3": {"reg_bits": 3},
-    # chunk groups (several passes per kernel over L2-resident chunks; auto from 24 qubits)
-    "chunk_13": {"chunk_qubits": 13},
-    "chunk_14_wide": {"tile_qubits": 12, "chunk_qubits": 14},
-    "chunk_16": {"chunk_qubits": 16},
-    "chunk_14_r3": {"chunk_qubits": 14, "reg_bits": 3},
+    "low_qubits_3": {"low_qubits": 3},
 }
 
 
@@ -78,7 +74,7 @@ def test_generated_kernel_variants_match_reference_golden(name, variant):
             eng.set_option(k, v)
         rep = _run(circ, theta, obs, inp, method)
     finally:
-        for k, v in {"jit": 1, "tile_qubits": 0, "tile_fwd": 0, "low_qubits": 3, "reg_bits": 0, "chunk_qubits": 0}.items():
+        for k, v in {"jit": 1, "tile_qubits": 0, "tile_fwd": 0, "low_qubits": 4, "reg_bits": 0}.items():
             eng.set_option(k, v)
     assert max_err(rep.values, cvec(gold["values"])) <= GRAD_TOL
     assert abs(rep.energy - complex(*gold["energy"])) <= ENERGY_TOL

@@ -156,54 +156,3 @@ def test_numeric_guard_rules():
     nu = sv.Gate(sv.NonUnitary(lambda: np.diag([1e300, 1.0]), 0), (0,))
     circ = sv.Circuit(6, (*w.circuit.gates, nu), w.circuit.num_params)
     _numeric_guard(circ, Problem(circ, w.theta, w.observable, sv.BasisState(6)), 1)  # may overflow: allowed
-
-
-def _chunked_plan(prob, tile, low, chunk):
-    import ctypes as C
-
-    lib = _native.load()
-    G = max(1, prob.c.num_gates)
-    order = np.zeros(G, dtype=np.int32)
-    start = np.zeros(G + 1, dtype=np.int32)
-    qmask = np.zeros(G, dtype=np.uint64)
-    group = np.zeros(G, dtype=np.int32)
-    cmask = np.zeros(G, dtype=np.uint64)
-    n = C.c_int32()
-    ptr = [C.c_void_p(a.ctypes.data) for a in (order, start, qmask, group, cmask)]
-    rc = lib.svg_debug_plan_chunked(C.byref(prob.c), tile, low, chunk, *ptr, C.byref(n))
-    assert rc == 0, lib.svg_last_error()
-    m = n.value
-    return order[: prob.c.num_gates], start[: m + 1], qmask[:m], group[:m], cmask[:m]
-
-
-@pytest.mark.parametrize("name,tile,low,chunk", [("cfg3_n14", 8, 3, 11), ("cfg4_n16", 8, 3, 10), ("cfg5_n15", 7, 3, 10),
-                                                 ("all_kinds_6_random", 3, 1, 5), ("cfg1", 7, 3, 9)])
-def test_chunk_groups_are_exact_reorderings(name, tile, low, chunk):
-    """Chunk-group schedules (several tile passes per kernel over L2-resident chunks):
-    each group's passes are consecutive, every member's tile lies inside the group's
-    chunk, and applying the gates in the planned order reproduces the reference's
-    gradient (the order only swaps commuting gates)."""
-    from emulator import emulate_order
-
-    rec = GOLD[name]
-    circ, theta, obs, inp, _ = materialize(CASES[name])
-    prob = lowering.Problem(circ, theta, obs, inp)
-    order, start, qmask, group, cmask = _chunked_plan(prob, tile, low, chunk)
-    assert sorted(order.tolist()) == list(range(len(circ.gates)))
-    seen = set()
-    for j in range(len(qmask)):
-        q, g = int(qmask[j]), int(group[j])
-        assert bin(q).count("1") == tile and q & ((1 << low) - 1) == (1 << low) - 1
-        if g >= 0:
-            c = int(cmask[j])
-            assert bin(c).count("1") == chunk and q & ~c == 0
-            assert g not in seen or int(group[j - 1]) == g  # members are consecutive
-            seen.add(g)
-        for gi in order[start[j]: start[j + 1]]:
-            gt = prob.gates[gi]
-            flip = int(gt["x_mask"]) if gt["form"] == _native.FORM_PAULI else sum(1 << t for t in gt["targets"][: gt["ntargets"]])
-            assert flip & ~q == 0
-    assert (group >= 0).any()
-    sums, energy = emulate_order(circ, theta, obs, inp, order)
-    assert max_err(2 * sums.real, cvec(rec["values"]).real) <= 1e-10
-    assert abs(energy - complex(*rec["energy"])) <= 1e-12
