@@ -192,13 +192,15 @@ int svg_engine_create_sharded(int device, int world, int rank, const uint8_t ncc
 int svg_engine_destroy(svg_engine* e);
 /* Launch on an external cudaStream_t (passed as void*); NULL = engine's own stream. */
 int svg_engine_set_stream(svg_engine* e, void* stream);
-/* Options (9): "tile_qubits" (0 = auto), "tile_fwd" (forward-only tile qubits, 0 auto, -1 off),
+/* Options (10): "tile_qubits" (0 = auto), "tile_fwd" (forward-only tile qubits, 0 auto, -1 off),
    "low_qubits" (3..5: contiguous low qubits every generated-kernel tile holds), "reg_bits"
    (0 auto, 3 or 4: 2^bits amplitudes per thread per buffer), "max_gates_per_pass" (0 = auto),
    "kernel" (0 auto, 1 shared-memory tiles, 2 register tiles), "jit" (circuit-specialised
    register-tile kernels compiled at run time with NVRTC: 0 off, 1 auto = shards of >= 10 qubits,
    2 always), "emulate_transport" (virtual engines: run the NCCL data path with device copies),
-   "profile" (1 = per-phase CUDA-event times in svg_stats). */
+   "profile" (1 = per-phase CUDA-event times in svg_stats), "checked" (generated kernels poison every
+   shared-memory element they read with NaN and bounds-check global tile indices: a read
+   ordering bug shows up as NaN in the results; debugging and tests only). */
 int svg_engine_set_option(svg_engine* e, const char* key, int64_t value);
 
 /* The hot path: one full adjoint sweep.  sums_out[num_params] receives the

@@ -195,6 +195,7 @@ struct svg_engine {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int64_t opt_tile = 0, opt_profile = 0, opt_max_items = 0, opt_kernel = 0, opt_reg_bits = 0;  // reg bits 0: auto
+  int64_t opt_checked = 0;  // generated kernels in checked mode (reg_ops.cuh SVGB_CHECK / poison2)
   // virtual engines: run the NCCL-mode data path (half-shard pack -> copy ->
   // unpack, partner fetch into scratch) with device copies as the transport
   int64_t opt_emulate_transport = 0;
@@ -1012,6 +1013,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.q = l.d.q;
         jp.swz = l.swz.col;
         jp.scale_carry = carry;
+        jp.checked = e->opt_checked != 0;
         jp.segs = L.segs.data() + l.d.seg_begin;
         jp.nsegs = l.d.seg_end - l.d.seg_begin;
         jp.rops = L.rops.data() + l.d.op_begin;
@@ -1444,6 +1446,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.q = l->d.q;
       jp.swz = l->swz.col;
       jp.scale_carry = carry;
+      jp.checked = e->opt_checked != 0;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -2117,6 +2120,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "tile_fwd") {
     if (value < -1 || value > 13) return fail(SVG_EINVAL, "tile_fwd must be in [-1, 13]");
     e->opt_tile_fwd = value;
+  } else if (k == "checked") {
+    e->opt_checked = value != 0;
   } else if (k == "low_qubits") {
     if (value < 3 || value > 5) return fail(SVG_EINVAL, "low_qubits must be in [3, 5]");
     e->opt_low_qubits = value;
@@ -2192,6 +2197,7 @@ extern "C" int svg_debug_jit_check(const svg_problem* p, const int64_t* opts, in
     if (opts) {
       e.opt_tile = opts[0];
       e.opt_reg_bits = opts[1];
+      e.opt_checked = opts[2];
     }
     (void)lower(&e, p, true);
     (void)cudaGetLastError();

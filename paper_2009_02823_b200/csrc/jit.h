@@ -31,6 +31,8 @@ struct JitPass {
   bool thread_acc = false, tiles = false;
   int acc_shift = 0;                 // thread_acc: lanes combined per accumulator (log2)
   bool scale_carry = false;          // deferred scale carried across layout changes (no shared-memory segments)
+  bool checked = false;              // checked mode: shared-memory reads poison what they read, global indices
+                                     // bounds-checked (reg_ops.cuh; debugging and tests only)
   uint64_t rest = 0;
   const uint8_t* q = nullptr;        // tile qubits (PassDesc.q)
   const uint8_t* swz = nullptr;      // shared-memory swizzle columns per tile position (engine.cu Swizzle)

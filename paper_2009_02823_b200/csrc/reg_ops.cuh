@@ -325,6 +325,32 @@ __device__ __forceinline__ void unstage(double2 (&v)[1 << R], const double2* stg
   for (int j = 0; j < (1 << R); ++j) v[j] = stg[j * nthr + tid];
 }
 
+// ---- checked mode (engine option "checked"; generated kernels only) ----
+// Shared-memory reads poison what they read with a NaN, so a read that comes
+// before its write in a later phase (a missing barrier or cp.async wait, a
+// wrong swizzle or staging slot) returns NaN and fails the parity check;
+// global tile indices are bounds-checked (trap).
+__device__ __forceinline__ double2 poison2() {
+  return make_double2(__longlong_as_double(0x7ff8dead0000beefll), __longlong_as_double(0x7ff8dead0000beefll));
+}
+#define SVGB_CHECK(cond) \
+  do {                   \
+    if (!(cond)) __trap(); \
+  } while (0)
+template <int R>
+__device__ __forceinline__ void unstage_poison(double2 (&v)[1 << R], double2* stg, int tid, int nthr) {
+#pragma unroll
+  for (int j = 0; j < (1 << R); ++j) {
+    v[j] = stg[j * nthr + tid];
+    stg[j * nthr + tid] = poison2();
+  }
+}
+// every global amplitude of a thread's 2^R slots lies below `limit`
+template <int R>
+__device__ __forceinline__ void check_rows(uint64_t row, const Map<R>& m, uint64_t limit) {
+  SVGB_CHECK(row + goff(m, (1 << R) - 1) < limit);
+}
+
 // One register op with its structure as template arguments (jit.cpp): the same
 // steps as the interpreted kernel's op loop, with every mask a literal.
 template <int R, int NB, int V, uint32_t XL, uint32_t ZLW, uint32_t CLW, uint32_t SMASK, uint32_t CMASK,

@@ -117,8 +117,8 @@ def test_non_pauli_observable_letters_expand_exactly():
     assert np.allclose(dense, dense_matrix(obs), atol=1e-15)
 
 
-@pytest.mark.parametrize("cfg,n,tile", [(2, 14, 0), (3, 20, 12), (5, 18, 0)])
-def test_generated_kernels_compile_for_sm100a(cfg, n, tile):
+@pytest.mark.parametrize("cfg,n,tile,checked", [(2, 14, 0, 0), (3, 20, 12, 0), (5, 18, 0, 0), (3, 16, 10, 1)])
+def test_generated_kernels_compile_for_sm100a(cfg, n, tile, checked):
     """Without a GPU: lower the config with circuit-specialised kernels forced on and
     NVRTC-compile every distinct generated pass kernel for sm_100a (free-lane
     layouts, swizzled transposes, tile-order staging, fused diagonal runs)."""
@@ -130,7 +130,7 @@ def test_generated_kernels_compile_for_sm100a(cfg, n, tile):
     lib = N.load()
     w = sv.build_workload(cfg, n)
     pr = Problem(w.circuit, w.theta, w.observable, sv.BasisState(n), real_sums=True)
-    opts = (C.c_int64 * 4)(tile, 0, 0, 0)
+    opts = (C.c_int64 * 4)(tile, 0, checked, 0)
     count = C.c_int32()
     rc = lib.svg_debug_jit_check(C.byref(pr.c), opts, C.byref(count))
     if rc != 0 and (b"NVRTC" in (lib.svg_last_error() or b"") or b"libnvrtc" in (lib.svg_last_error() or b"")):
