@@ -407,9 +407,26 @@ def _measure(args, w, eng, sharded, rank, world, local_rank, dist, steps, warmup
     torch.cuda.synchronize()
 
     e2e = None
+    local = (1 << n) // world if sharded else (1 << n)
+    if with_e2e:
+        # every rank of this node pins its host input: skip the e2e leg (all ranks
+        # together) when the node's free memory cannot hold them with headroom
+        need = 16 * local * (world if dist else 1)
+        try:
+            with open("/proc/meminfo") as f:
+                avail = next(int(l.split()[1]) * 1024 for l in f if l.startswith("MemAvailable"))
+        except Exception:
+            avail = need * 2
+        ok = avail > 1.5 * need
+        if dist:
+            t = torch.tensor([1.0 if ok else 0.0], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok = bool(t.item() > 0.5)
+        if not ok:
+            e2e = {"skipped": f"pinned host inputs of {need / 2**30:.0f} GiB exceed the node's free memory"}
+            with_e2e = False
     if with_e2e:
         # pinned host input: the whole state (one process) or this rank's slice (sharded)
-        local = (1 << n) // world if sharded else (1 << n)
         pinned = torch.empty(local, dtype=torch.complex128, pin_memory=True)
         host = pinned.numpy()
         host[:] = 0
@@ -506,7 +523,7 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(w)
     e2e = m["e2e"]
-    if e2e is not None:
+    if e2e is not None and "value" in e2e:
         e2e["value"] *= jobs
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -20,8 +20,8 @@ CASES = {**small_cases(), **config_cases()}
 
 
 @pytest.mark.parametrize("name,tile,reg_bits", [("cfg3_n14", 9, 4), ("cfg3_n14", 10, 3), ("cfg5_n15", 10, 4),
-                                                ("cfg4_n16", 12, 4), ("cfg2_n12", 8, 3), ("all_kinds_6_random", 0, 0),
-                                                ("family_D9_random", 7, 0), ("cfg5_n15", 7, 3)])
+                                                ("cfg4_n16", 12, 4), ("cfg2_n12", 8, 3), ("cfg1", 0, 0),
+                                                ("family_D9_random", 9, 4), ("cfg5_n15", 8, 3)])
 def test_checked_generated_kernels(name, tile, reg_bits):
     rec = GOLD[name]
     circ, theta, obs, inp, _ = materialize(CASES[name])
