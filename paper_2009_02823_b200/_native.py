@@ -70,11 +70,13 @@ class svg_problem(C.Structure):
     _fields_ = [
         ("num_qubits", C.c_int32), ("num_params", C.c_int32), ("num_gates", C.c_int32),
         ("num_derivs", C.c_int32), ("num_terms", C.c_int32), ("flags", C.c_int32),
-        ("gates", C.POINTER(svg_gate)), ("derivs", C.POINTER(svg_deriv)),
-        ("terms", C.POINTER(svg_pauli_term)), ("input_basis", C.c_int64),
+        # table pointers held as addresses (c_void_p): assigning a numpy array's
+        # .ctypes.data is ~10x cheaper per call than data_as(POINTER(...))
+        ("gates", C.c_void_p), ("derivs", C.c_void_p),
+        ("terms", C.c_void_p), ("input_basis", C.c_int64),
         ("input_amps", C.c_void_p),
         ("num_product_terms", C.c_int32), ("num_factors", C.c_int32),
-        ("product_terms", C.POINTER(svg_product_term)), ("factors", C.POINTER(svg_factor)),
+        ("product_terms", C.c_void_p), ("factors", C.c_void_p),
     ]
 
 

@@ -709,10 +709,12 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   L.b = (nloc <= L.k) ? nloc : std::min(5, L.k - 2);
   if (g > 0 && L.b < 5 && nloc > L.k) throw InvalidArg("sharded engines need >= 7 qubits per shard");
   // register bits (amplitudes per thread per buffer = 2^R): auto = 4 for the
-  // generated kernels (fewer ops per amplitude; measured cfg 2 / cfg 3); the
+  // generated kernels (fewer ops per amplitude; measured cfg 2 / cfg 3) unless the
+  // whole state is one tile -- then a pass is one CTA on one SM, and twice the warps
+  // hide more latency (cfg 1: 6416 vs 5088 gradients/s at R = 3 / 4); the
   // interpreter keeps 3 for shards of <= 23 qubits (more threads per tile: better
   // latency hiding when a pass is only a few tile rounds)
-  const int Rauto = (nloc <= 23 && !jit_expected) ? 3 : 4;
+  const int Rauto = (nloc <= 23 && !jit_expected) || (jit_expected && nloc <= L.k) ? 3 : 4;
   const int RB = e->opt_reg_bits ? static_cast<int>(e->opt_reg_bits) : Rauto;          // reverse passes
   const int RF = RB;  // forward passes
   L.R = RB;
@@ -1656,7 +1658,11 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     for (const Launch& l : L.obs) multi_pass_products = multi_pass_products || (l.kind == L_PROD && !l.prod.last);
     if (multi_pass_products) e->prodbuf.reserve(amps * sizeof(double2));
     if (e->comm) {
-      e->scratch.reserve(shard_amps * sizeof(double2));
+      // exchange staging: one shard (partner fetch / one buffer's swap), two when the
+      // reverse sweep swaps phi and lambda together
+      bool rev_swaps = false;
+      for (const Launch& l : L.rev) rev_swaps = rev_swaps || l.kind == L_SWAP;
+      e->scratch.reserve((rev_swaps ? 2 : 1) * shard_amps * sizeof(double2));
       e->gathered.reserve(cnt * world * sizeof(double2));
     }
 
@@ -1719,6 +1725,28 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       nccl->check(nccl->recv(recv, half_bytes, kNcclUint8, partner, e->comm, s), "ncclRecv");
       nccl->check(nccl->group_end(), "ncclGroupEnd");
       launch_half_unpack(recv, buf, nloc, lpos, 1 - a, s);
+    };
+    // reverse-sweep swaps exchange phi AND lambda: over NCCL both halves go out in
+    // one group (two concurrent transfers per partner instead of two back-to-back
+    // exchanges); scratch holds [phi send | phi recv | lambda send | lambda recv]
+    auto swap_pair = [&](int gbit, int lpos) {
+      if (!e->comm) {
+        swap_buffer(psi, gbit, lpos);
+        swap_buffer(lam, gbit, lpos);
+        return;
+      }
+      const int a = (e->rank >> gbit) & 1, partner = e->rank ^ (1 << gbit);
+      const size_t h = shard_amps / 2;
+      launch_half_pack(psi, scratch, nloc, lpos, 1 - a, s);
+      launch_half_pack(lam, scratch + 2 * h, nloc, lpos, 1 - a, s);
+      nccl->check(nccl->group_start(), "ncclGroupStart");
+      nccl->check(nccl->send(scratch, half_bytes, kNcclUint8, partner, e->comm, s), "ncclSend");
+      nccl->check(nccl->recv(scratch + h, half_bytes, kNcclUint8, partner, e->comm, s), "ncclRecv");
+      nccl->check(nccl->send(scratch + 2 * h, half_bytes, kNcclUint8, partner, e->comm, s), "ncclSend");
+      nccl->check(nccl->recv(scratch + 3 * h, half_bytes, kNcclUint8, partner, e->comm, s), "ncclRecv");
+      nccl->check(nccl->group_end(), "ncclGroupEnd");
+      launch_half_unpack(scratch + h, psi, nloc, lpos, 1 - a, s);
+      launch_half_unpack(scratch + 3 * h, lam, nloc, lpos, 1 - a, s);
     };
     auto fetch_partner = [&](uint64_t xglob) {  // partner shard's psi -> scratch (NCCL mode)
       const int partner = e->rank ^ static_cast<int>(xglob >> nloc);
@@ -1848,8 +1876,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     CK(cudaEventRecord(e->ev[3], s));
     for (const Launch& l : L.rev) {
       if (l.kind == L_SWAP) {
-        swap_buffer(psi, l.gbit, l.lpos);
-        swap_buffer(lam, l.gbit, l.lpos);
+        swap_pair(l.gbit, l.lpos);
         continue;
       }
       for (int sh = 0; sh < nsh; ++sh) {

@@ -34,6 +34,7 @@ import numpy as np
 from . import _native as N
 from .ir import NonInvertibleGateError, SIGMA, bound_matrix, derivative_scale, invert_small, kind_name, matrix_derivative
 from .operators import FACTOR_MATRICES, pauli_masks, pauli_strings, split_terms
+from .state import ShardSlice, basis_index_of
 
 GATE_DTYPE = np.dtype(  # itemsize 816 = 51 complex128 slots (bind scatters into a flat complex view)
     [
@@ -163,28 +164,32 @@ def bind(circuit, params: np.ndarray, forward_only: bool = False) -> tuple[np.nd
         if len(tls) > 16:
             tls.clear()
         g, d = st.gates.copy(), st.derivs.copy()
-        # the rotation coefficients a, b of (fwd, rewind, adjoint) as positions in a
-        # flat complex view of the gate records: one scatter per call
-        flat = g.view(np.complex128).reshape(-1)
-        rec = GATE_DTYPE.itemsize // 16
-        base = st.rot_gates * rec
-        pos = np.concatenate([base + (GATE_DTYPE.fields[f][1] // 16) + j
-                              for f in ("fwd", "rewind", "adjoint") for j in (0, 1)])
-        hit = tls[id(st)] = (st, g, d, flat, pos, d["k"], d["basis"])
-    gates, derivs, flat, pos, dk, dbasis = hit[1:]
+        # the rotation coefficients a = cos, b = i sin of (fwd, rewind, adjoint) as
+        # positions in a flat float64 view of the gate records (imag(a) = re(b) = 0
+        # from the structure): three scatters per call, no temporaries
+        fl = g.view(np.float64).reshape(-1)
+        base = st.rot_gates * (GATE_DTYPE.itemsize // 8)
+        off = {f: GATE_DTYPE.fields[f][1] // 8 for f in ("fwd", "rewind", "adjoint")}
+        re_a = np.stack([base + off[f] for f in ("fwd", "rewind", "adjoint")])   # real(a), 3 x nrot
+        im_b = base + off["fwd"] + 3                                              # imag(b) of U
+        im_bc = np.stack([base + off[f] + 3 for f in ("rewind", "adjoint")])     # imag(b) of U^dag
+        for field in ("fwd", "rewind", "adjoint"):  # fixed X/Y/Z: a = 0, b = 1
+            g[field][st.fixed_pauli, 1] = 1.0
+        d["basis"][st.rot_derivs] = 1  # rotation generators in the post-gate basis
+        hit = tls[id(st)] = [st, g, d, fl, re_a, im_b, im_bc, d["k"], None]
+    _, gates, derivs, fl, re_a, im_b, im_bc, dk, last_scale = hit
     scale = derivative_scale()
     if st.rot_gates.size:
         ang = st.rot_alpha * params[st.rot_refs]
-        a = np.cos(ang) + 0j
-        b = 1j * np.sin(ang)
-        ca, cb = np.conj(a), np.conj(b)
-        flat[pos] = np.concatenate((a, b, ca, cb, ca, cb))  # fwd, rewind, adjoint
-        # post-gate generator (basis 1): dU phi_i = alpha*i P U phi_i = alpha*i P phi_{i+1}
-        dk[st.rot_derivs, 1] = (st.rot_alpha * 1j) * scale
-        dbasis[st.rot_derivs] = 1
-    if st.fixed_pauli.size:
-        for field in ("fwd", "rewind", "adjoint"):
-            gates[field][st.fixed_pauli, 1] = 1.0
+        c, sn = np.cos(ang), np.sin(ang)
+        fl[re_a] = c
+        fl[im_b] = sn
+        np.negative(sn, out=sn)
+        fl[im_bc] = sn
+        if scale != last_scale:
+            # post-gate generator (basis 1): dU phi_i = alpha*i P U phi_i = alpha*i P phi_{i+1}
+            dk[st.rot_derivs, 1] = (st.rot_alpha * 1j) * scale
+            hit[8] = scale
     if st.mat_gates:
         first = np.concatenate([[0], np.cumsum(gates["nderiv"])])
         for i in st.mat_gates:
@@ -265,10 +270,6 @@ class Problem:
         self.gates, self.derivs = bind(circuit, params, forward_only)
         self.terms, self.products, self.factors = lower_terms(obs)
         self.num_derivs = len(self.derivs)
-        from .state import basis_index_of
-
-        from .state import ShardSlice
-
         basis = basis_index_of(input_state)
         self.amps = None
         local = isinstance(input_state, ShardSlice)
@@ -281,13 +282,13 @@ class Problem:
         p.num_derivs = self.num_derivs
         p.num_terms = len(self.terms)
         p.flags = (FLAG_REAL_SUMS if real_sums else 0) | (FLAG_INPUT_LOCAL if local else 0)
-        p.gates = self.gates.ctypes.data_as(C.POINTER(N.svg_gate))
-        p.derivs = self.derivs.ctypes.data_as(C.POINTER(N.svg_deriv))
-        p.terms = self.terms.ctypes.data_as(C.POINTER(N.svg_pauli_term))
+        p.gates = self.gates.ctypes.data
+        p.derivs = self.derivs.ctypes.data
+        p.terms = self.terms.ctypes.data
         p.num_product_terms = len(self.products)
         p.num_factors = len(self.factors)
-        p.product_terms = self.products.ctypes.data_as(C.POINTER(N.svg_product_term))
-        p.factors = self.factors.ctypes.data_as(C.POINTER(N.svg_factor))
+        p.product_terms = self.products.ctypes.data
+        p.factors = self.factors.ctypes.data
         p.input_basis = 0 if basis is None else basis
         p.input_amps = None if self.amps is None else self.amps.ctypes.data
         self.c = p
