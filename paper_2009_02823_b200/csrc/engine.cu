@@ -203,9 +203,11 @@ struct svg_engine {
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
+  int64_t opt_windows = 1;       // pass planner: also try windows of contiguous qubits (plan_best_pass)
   int64_t opt_low_qubits = 4;    // generated kernels: contiguous low qubits every tile holds (3..5)
   mutable std::string jit_error;
-  bool jit_dry_run = false;        // svg_debug_jit_check
+  int jit_dry_run = 0;             // svg_debug_jit_check (1), svg_debug_plan_stats (2: no compile)
+  mutable double plan_stats[16] = {};
   mutable int jit_dry_count = 0;
   // occupancy queries are driver calls: memoised per (kernel kind, R, threads, smem)
   mutable std::map<std::tuple<int, int, int, size_t>, int> occ_memo;
@@ -626,9 +628,9 @@ bool reg_capable(const svg_gate& g, uint32_t flip_tile) {
 
 std::vector<Segment> memo_segments(const svg_engine* e, const std::vector<uint32_t>& flips,
                                    const std::vector<uint32_t>& touch, const std::vector<char>& dense, int k,
-                                   int regbits, bool free = false) {
+                                   int regbits, bool free = false, int lowb = 5) {
   Hasher h;
-  const int32_t head[] = {k, regbits, free ? 1 : 0, static_cast<int32_t>(flips.size())};
+  const int32_t head[] = {k, regbits, free ? 1 + lowb : 0, static_cast<int32_t>(flips.size())};
   h.pod(head);
   h.bytes(flips.data(), flips.size() * 4);
   h.bytes(touch.data(), touch.size() * 4);
@@ -636,7 +638,8 @@ std::vector<Segment> memo_segments(const svg_engine* e, const std::vector<uint32
   const Key128 key = h.key();
   auto it = e->seg_memo.find(key);
   if (it != e->seg_memo.end()) return it->second;
-  std::vector<Segment> segs = free ? plan_segments_free(flips, touch, k, regbits) : plan_segments(flips, touch, dense, k, regbits);
+  std::vector<Segment> segs =
+      free ? plan_segments_free(flips, touch, k, regbits, lowb) : plan_segments(flips, touch, dense, k, regbits);
   if (e->seg_memo.size() > 16384) e->seg_memo.clear();
   e->seg_memo.emplace(key, segs);
   return segs;
@@ -744,6 +747,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     pp.max_items = static_cast<int>(e->opt_max_items);
   else if (L.reg)
     pp.max_items = kRegPassGates;
+  pp.windows = e->opt_windows != 0;
   const int64_t S = int64_t(16) << nloc;  // bytes of one state shard
 
   std::vector<GateShape> logical(p->num_gates);
@@ -752,7 +756,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // the schedule is a pure function of the gate shapes and plan parameters: memoised
   auto schedule = [&](const PlanParams& pq, std::vector<int>* l2p_out) {
     Hasher h;
-    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs, static_cast<int32_t>(logical.size())};
+    const int32_t head[] = {n, g, pq.n, pq.k, pq.b, pq.max_items, pq.max_derivs, pq.windows, static_cast<int32_t>(logical.size())};
     h.pod(head);
     for (const GateShape& sh : logical) {
       h.word(sh.flip);
@@ -842,6 +846,11 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // free-lane plans also need tile staging (a first segment off the global
   // layout reads its tile from the staged copy)
   const bool free_lanes = jit_planned;
+  // Tile rows are 2^L.b contiguous amplitudes: a layout whose lanes include tile
+  // positions 0..lowb-1 loads and stores whole rows whatever its other lanes hold,
+  // so (generated kernels, L.b < 5) it needs no transpose back to positions 0..4
+  const int lowb = std::min(5, L.b);
+  const uint32_t lowmask = (1u << lowb) - 1u;
   // segments of one pass at tile width kk with R register bits: the fixed-lane
   // plan, or the free-lane plan when the cost model prefers it (lc: lane op,
   // xc: layout change, in register-op units)
@@ -857,7 +866,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     }
     // the choice (plan + swizzle) is memoised per pass structure and cost model
     Hasher h;
-    const int32_t head[] = {kk, R, free_lanes ? 1 : 0, static_cast<int32_t>(flips.size())};
+    const int32_t head[] = {kk, R, free_lanes ? 1 + lowb : 0, static_cast<int32_t>(flips.size())};
     h.pod(head);
     h.pod(lc);
     h.pod(xc);
@@ -877,8 +886,8 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
     bool free_ok = free_lanes;
     for (size_t j = 0; j < ps.items.size() && free_ok; ++j) free_ok = !dense[j] && __builtin_popcount(flips[j]) <= 1;
     if (free_ok) {
-      std::vector<Segment> fr = memo_segments(e, flips, touch, dense, kk, R, true);
-      if (segment_plan_cost(fr, flips, lc, xc) < segment_plan_cost(*out, flips, lc, xc)) *out = std::move(fr);
+      std::vector<Segment> fr = memo_segments(e, flips, touch, dense, kk, R, true, lowb);
+      if (segment_plan_cost(fr, flips, lc, xc, lowb) < segment_plan_cost(*out, flips, lc, xc, lowb)) *out = std::move(fr);
     }
     std::vector<uint32_t> ls;
     for (const Segment& sg : *out) {
@@ -977,7 +986,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         }
         L.segs.push_back(sd);
       }
-      if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
+      if (prev_l != ~0u && (prev_l & lowmask) != lowmask) {  // back to the global lane layout for the store
         SegLocal sl;
         SegDesc sd = make_seg(SEG_REG, default_regs(RF), 31u, l.swz, kf, RF, &sl);
         sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
@@ -1016,6 +1025,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.swz = l.swz.col;
         jp.scale_carry = carry;
         jp.checked = e->opt_checked != 0;
+        jp.lowb = std::min(5, L.b);
         jp.segs = L.segs.data() + l.d.seg_begin;
         jp.nsegs = l.d.seg_end - l.d.seg_begin;
         jp.rops = L.rops.data() + l.d.op_begin;
@@ -1299,7 +1309,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
           }
           L.segs.push_back(sd);
         }
-        if (prev_l != ~0u && prev_l != 31u) {  // back to the global lane layout for the store
+        if (prev_l != ~0u && (prev_l & lowmask) != lowmask) {  // back to the global lane layout for the store
           SegLocal sl;
           SegDesc sd = make_seg(SEG_REG, default_regs(RB), 31u, l.swz, L.k, RB, &sl);
           sd.op_begin = sd.op_end = static_cast<int>(L.rops.size());
@@ -1449,6 +1459,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.swz = l->swz.col;
       jp.scale_carry = carry;
       jp.checked = e->opt_checked != 0;
+      jp.lowb = std::min(5, L.b);
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -1456,6 +1467,26 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       passes.push_back(jp);
     }
     try {
+      if (e->jit_dry_run == 2) {  // svg_debug_plan_stats: the plan's shape, nothing generated
+        double* st = e->plan_stats;
+        for (const Launch* l : regl) {
+          const int o = l->nb == 2 ? 8 : 0;
+          st[o + 0] += 1;  // passes
+          for (int si = l->d.seg_begin; si < l->d.seg_end; ++si) {
+            const SegDesc& sg = L.segs[si];
+            st[o + 1] += 1;                                                      // segments
+            if (si > l->d.seg_begin && !(sg.kind == SEG_REG && sg.same_map)) st[o + 2] += 1;  // layout changes
+            if (sg.kind != SEG_REG) continue;
+            for (int oi = sg.op_begin; oi < sg.op_end; ++oi) {
+              st[o + 3] += 1;                                                    // register ops
+              if (L.rops[oi].xl) st[o + 4] += 1;                                 // lane flips
+            }
+          }
+          st[o + 5] = std::max(st[o + 5], double(l->d.nslots));
+          if (l->d.acc_shift) st[o + 6] += 1;                                    // passes with lane-group accumulators
+        }
+        throw std::runtime_error("dry run");
+      }
       std::string why;
       if (!jit_available(&why)) throw std::runtime_error(why);
       std::vector<std::shared_ptr<JitKernel>> ks = jit_get(passes, e->jit_dry_run ? -1 : e->device);
@@ -2155,6 +2186,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "jit") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "jit must be 0 (off), 1 (auto) or 2 (always)");
     e->opt_jit = value;
+  } else if (k == "pass_windows") {
+    e->opt_windows = value != 0;
   } else if (k == "max_gates_per_pass") {
     if (value < 0) return fail(SVG_EINVAL, "max_gates_per_pass must be >= 0");
     e->opt_max_items = value;
@@ -2230,6 +2263,35 @@ extern "C" int svg_debug_jit_check(const svg_problem* p, const int64_t* opts, in
     (void)cudaGetLastError();
     if (npasses) *npasses = e.jit_dry_count;
     if (e.jit_error != "dry run") return fail(SVG_EINVAL, "generated kernels: " + e.jit_error);
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_EINVAL, ex.what());
+  }
+}
+
+// Debug / tools (not in the public header): the shape of the plan the engine would
+// run with generated kernels (no GPU, nothing compiled).  opts: tile_qubits, reg_bits,
+// low_qubits, max_gates_per_pass, pass_windows (0/1), log2(shards).  out[0..7] forward,
+// out[8..15] reverse: passes, segments, layout changes, register ops, lane flips,
+// max slots, passes with lane-group accumulators.
+extern "C" int svg_debug_plan_stats(const svg_problem* p, const int64_t* opts, double* out) {
+  try {
+    validate(p);
+    svg_engine e;
+    e.sms = 148;
+    e.max_smem = 232448;
+    e.max_smem_sm = 233472;
+    e.opt_jit = 2;
+    e.jit_dry_run = 2;
+    e.opt_tile = opts[0];
+    e.opt_reg_bits = opts[1];
+    if (opts[2]) e.opt_low_qubits = opts[2];
+    e.opt_max_items = opts[3];
+    e.opt_windows = opts[4];
+    e.shard_bits = static_cast<int>(opts[5]);
+    (void)lower(&e, p, true);
+    (void)cudaGetLastError();
+    for (int i = 0; i < 16; ++i) out[i] = e.plan_stats[i];
     return SVG_OK;
   } catch (const std::exception& ex) {
     return fail(SVG_EINVAL, ex.what());

@@ -26,7 +26,7 @@ static uint64_t pad_tile(uint64_t q, int n, int k) {
 }
 
 Pass plan_one_pass(const std::vector<GateShape>& shapes, std::vector<char>& done, const PlanParams& pp,
-                   uint64_t forbidden_flip) {
+                   uint64_t forbidden_flip, uint64_t allowed_flip) {
   const int G = static_cast<int>(shapes.size());
   // every qubit counts for the early exit, including global (rank) positions
   uint64_t all = 0;
@@ -39,7 +39,8 @@ Pass plan_one_pass(const std::vector<GateShape>& shapes, std::vector<char>& done
     if (done[i]) continue;
     const GateShape& s = shapes[i];
     const uint64_t diag = s.touch & ~s.flip;
-    bool ok = !(s.touch & flip_blocked) && !(s.flip & diag_blocked) && !(s.flip & forbidden_flip);
+    bool ok = !(s.touch & flip_blocked) && !(s.flip & diag_blocked) && !(s.flip & forbidden_flip) &&
+              !(s.flip & ~allowed_flip);
     ok = ok && popc(q | s.flip) <= pp.k;
     ok = ok && static_cast<int>(p.items.size()) < pp.max_items;
     ok = ok && derivs + s.nderiv <= pp.max_derivs;
@@ -58,12 +59,49 @@ Pass plan_one_pass(const std::vector<GateShape>& shapes, std::vector<char>& done
   return p;
 }
 
+// The pass that takes the most gates among the plain greedy one (its tile grows
+// with the gate order: layer by layer, a strip of the circuit per pass) and the
+// greedy passes restricted to a window of qubits contiguous in logical order
+// (plus the forced low qubits).  On layered nearest-neighbour circuits a fixed
+// window holds a parallelogram of the circuit -- several layers deep, shifted by
+// the light cone -- instead of one layer's strip: fewer HBM passes.
+Pass plan_best_pass(const std::vector<GateShape>& shapes, std::vector<char>& done, const PlanParams& pp,
+                    uint64_t forbidden_flip, const std::vector<int>* l2p) {
+  std::vector<char> best_done = done;
+  Pass best = plan_one_pass(shapes, best_done, pp, forbidden_flip);
+  if (pp.windows && !best.items.empty()) {
+    int nq = 0;  // qubits in logical order (physical positions through l2p)
+    for (const GateShape& s : shapes)
+      if (s.touch) nq = std::max(nq, 64 - __builtin_clzll(s.touch));
+    if (l2p) nq = static_cast<int>(l2p->size());
+    auto phys = [&](int q) { return l2p ? (*l2p)[q] : q; };
+    uint64_t seen = 0;
+    for (int a = 0; a < nq; ++a) {
+      uint64_t w = low_mask(pp.b);
+      for (int q = a; q < nq && popc(w) < pp.k; ++q) {
+        const uint64_t bit = 1ull << phys(q);
+        if (!(bit & forbidden_flip)) w |= bit;
+      }
+      if (w == seen) continue;
+      seen = w;
+      std::vector<char> trial = done;
+      Pass p = plan_one_pass(shapes, trial, pp, forbidden_flip, w);
+      if (p.items.size() > best.items.size()) {
+        best = std::move(p);
+        best_done.swap(trial);
+      }
+    }
+  }
+  done.swap(best_done);
+  return best;
+}
+
 std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const PlanParams& pp) {
   std::vector<char> done(shapes.size(), 0);
   std::vector<Pass> passes;
   size_t placed = 0;
   while (placed < shapes.size()) {
-    Pass p = plan_one_pass(shapes, done, pp, 0);
+    Pass p = plan_best_pass(shapes, done, pp, 0, nullptr);
     if (p.items.empty()) throw std::runtime_error("planner made no progress (gate flip set wider than tile)");
     placed += p.items.size();
     passes.push_back(std::move(p));
@@ -99,7 +137,7 @@ std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, in
   int placed = 0, swaps_in_a_row = 0;
   while (placed < G) {
     std::vector<char> trial = done;
-    Pass p = plan_one_pass(phys, trial, pp, rank_mask);
+    Pass p = plan_best_pass(phys, trial, pp, rank_mask, &l2p);
     if (!p.items.empty()) {
       done.swap(trial);
       placed += static_cast<int>(p.items.size());
@@ -292,9 +330,10 @@ std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const 
 }
 
 std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
-                                        int k, int regbits) {
+                                        int k, int regbits, int lowb) {
   const int m = static_cast<int>(flip_pos.size());
   const uint32_t all = (k >= 32) ? ~0u : ((1u << k) - 1);
+  const uint32_t low = (1u << lowb) - 1u;  // positions whose lanes keep global rows contiguous
   std::vector<std::vector<int>> succ(m);
   std::vector<int> npred(m, 0);
   for (int i = 0; i < m; ++i)
@@ -338,7 +377,7 @@ std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, c
       for (uint32_t v = cand; v; v &= v - 1) {
         const int p = __builtin_ctz(v);
         const int c = closure(regs | (1u << p), nullptr);
-        if (c > best || (c == best && p >= 5 && best_pos < 5)) {  // ties: keep 0..4 free for the lanes
+        if (c > best || (c == best && p >= lowb && best_pos < lowb)) {  // ties: keep the low positions free for the lanes
           best = c;
           best_pos = p;
         }
@@ -373,7 +412,8 @@ std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, c
     uint32_t& rm = segs[s].regmask;
     for (size_t t = s + 1; t < segs.size() && popc(rm) < regbits; ++t)
       for (uint32_t v = segs[t].regmask & ~rm; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
-    for (uint32_t v = all & ~rm & ~31u; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+    for (uint32_t v = all & ~rm & ~low & ~31u; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
+    for (uint32_t v = all & ~rm & ~low; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
     for (uint32_t v = all & ~rm; v && popc(rm) < regbits; v &= v - 1) rm |= v & (~v + 1);
     uint32_t lanes = 31u & ~rm;
     for (uint32_t v = all & ~rm & ~lanes; v && popc(lanes) < 5; v &= v - 1) lanes |= v & (~v + 1);
@@ -383,7 +423,8 @@ std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, c
 }
 
 double segment_plan_cost(const std::vector<Segment>& segs, const std::vector<uint32_t>& flip_pos, double lane_cost,
-                         double xpose_cost) {
+                         double xpose_cost, int lowb) {
+  const uint32_t low = (1u << lowb) - 1u;
   double c = 0.0;
   uint32_t prev_r = ~0u, prev_l = ~0u;
   for (size_t s = 0; s < segs.size(); ++s) {
@@ -397,8 +438,8 @@ double segment_plan_cost(const std::vector<Segment>& segs, const std::vector<uin
       c += f == 0 ? 0.5 : ((f & sg.lanemask) ? lane_cost : 1.0);
     }
   }
-  if (!segs.empty() && segs.back().lanemask != 31u) c += xpose_cost;   // forward store
-  if (!segs.empty() && segs.front().lanemask != 31u) c += xpose_cost;  // reverse store
+  if (!segs.empty() && (segs.back().lanemask & low) != low) c += xpose_cost;   // forward store
+  if (!segs.empty() && (segs.front().lanemask & low) != low) c += xpose_cost;  // reverse store
   return c;
 }
 

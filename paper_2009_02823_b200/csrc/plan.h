@@ -41,6 +41,7 @@ struct PlanParams {
   int b = 5;                 // forced contiguous low qubits
   int max_items = 256;       // gates per pass cap
   int max_derivs = 96;       // derivative slots per pass cap (shared-memory accumulators)
+  int windows = 1;           // also try passes restricted to windows of contiguous qubits (plan_best_pass)
 };
 
 GateShape gate_shape(const svg_gate& g);
@@ -51,8 +52,13 @@ std::vector<Pass> plan_gate_passes(const std::vector<GateShape>& shapes, const P
 // One greedy pass over the not-yet-`done` gates (marks the gates it takes).
 // Gates flipping a `forbidden_flip` position (a sharded qubit) are skipped and
 // block their qubits like any other excluded gate.
+// Only gates whose flips lie in `allowed_flip` are taken (the others block).
 Pass plan_one_pass(const std::vector<GateShape>& shapes, std::vector<char>& done, const PlanParams& pp,
-                   uint64_t forbidden_flip);
+                   uint64_t forbidden_flip, uint64_t allowed_flip = ~0ull);
+// The best of the plain greedy pass and the greedy passes over windows of qubits
+// contiguous in logical order (l2p: logical -> physical, or null for the identity).
+Pass plan_best_pass(const std::vector<GateShape>& shapes, std::vector<char>& done, const PlanParams& pp,
+                    uint64_t forbidden_flip, const std::vector<int>* l2p);
 
 // Observable passes: terms grouped so each pass's flip masks fit one tile.
 // Terms whose flip mask cannot share a tile with the low qubits go to `direct`
@@ -80,16 +86,18 @@ std::vector<Segment> plan_segments(const std::vector<uint32_t>& flip_pos, const 
 // gates flip register positions only -- no lane flips (a lane flip is a warp
 // shuffle of both buffers, ~3.7x a register op).  Lanes are 5 positions the
 // segment does not flip, preferring tile positions 0..4 (the global layout).
-// Layout changes go through shared memory (transposes).
+// Layout changes go through shared memory (transposes).  `lowb`: tile positions
+// 0..lowb-1 are the contiguous low qubits of a global tile row; a layout whose
+// lanes include them loads and stores whole rows whatever its other lanes are.
 std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, const std::vector<uint32_t>& touch_pos,
-                                        int k, int regbits);
+                                        int k, int regbits, int lowb = 5);
 
 // Relative cost of a segment plan in register-op units (nb buffers): register
 // flips 1, lane flips `lane_cost`, diagonal ops 0.5, each layout change
-// `xpose_cost`; `std_end` adds a final transpose when the last segment's
-// lanes are not tile positions 0..4 (the store needs the global layout).
+// `xpose_cost`, plus a final transpose when the last segment's lanes do not
+// include tile positions 0..lowb-1 (the store needs whole global rows).
 double segment_plan_cost(const std::vector<Segment>& segs, const std::vector<uint32_t>& flip_pos, double lane_cost,
-                         double xpose_cost);
+                         double xpose_cost, int lowb = 5);
 
 // ---- sharded schedules (state split over 2^g ranks by its top g PHYSICAL qubits) ----
 //
