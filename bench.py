@@ -519,6 +519,8 @@ def run_ours(args, rank, world, local_rank):
     value = jobs * args.steps / (total_ms * 1e-3)
     B_alg = 6 * w.num_gates * S  # gate-level algorithmic bytes per gradient
     n_param_gates = sum(1 for g in w.circuit.gates if len(g.param_refs) > 0)
+    fp64_floor_ms = (12 * (S_rank // 16) * n_param_gates / max(1, int(st_last["rev_passes"]))
+                     / (FP64_PEAK_TFLOPS * 1e12) * 1e3)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(w)
@@ -544,6 +546,11 @@ def run_ours(args, rank, world, local_rank):
             "traffic": traffic, "kernel": "fused reverse register-tile pass (generated svgb_jit)",
             "bytes_per_launch": 4 * S_rank,
             "avg_launch_ms": avg_launch_ms, "peak_source": peak_src,
+            # a reverse pass fuses ~50 gates: its FP64 floor (6 DFMA per amplitude and
+            # parametrised gate at the measured DFMA peak) is of the order of its HBM floor
+            "hbm_floor_ms": 4 * S_rank / (peak * 1e9) * 1e3,
+            "fp64_floor_ms": fp64_floor_ms,
+            "frac_of_binding_floor": max(4 * S_rank / (peak * 1e9) * 1e3, fp64_floor_ms) / avg_launch_ms,
         },
         # the reverse sweep's algorithmic FP64 work: 6 FMA (12 flop) per amplitude per
         # parametrised gate (rewind phi and lambda: 2 FMA each, Re<lambda|K|phi>: 2),

@@ -203,6 +203,7 @@ struct svg_engine {
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
+  int64_t opt_slot_cap = 1;      // (tuning) cap a pass's derivative slots at the per-thread accumulator budget
   int64_t opt_windows = 1;       // pass planner: also try windows of contiguous qubits (plan_best_pass)
   int64_t opt_low_qubits = 4;    // generated kernels: contiguous low qubits every tile holds (3..5)
   mutable std::string jit_error;
@@ -489,9 +490,12 @@ constexpr double kMinDeferredC = 1e-60;
 // many qubits (measured 1.8-2x the interpreter's gradients/s from 10 qubits on;
 // below 10 the first call's compile outweighs the few microseconds of work).
 constexpr int kJitMinQubits = 10;
-// Gates per register-tile pass: beyond ~40 the straight-line pass kernels
-// outgrow the instruction cache (measured: cfg 3 reverse 115 ms at 96, 105 ms at 40).
-constexpr int kRegPassGates = 40;
+// Gates per register-tile pass.  With the window planner a pass holds a
+// parallelogram of the circuit several layers deep, so the cap (with the slot
+// cap below) sets the number of HBM passes: measured cfg 4 (n = 30) 0.94 / 1.01 /
+// 1.05 / 1.06 gradients/s at 44 / 48 / 64 / 72 (36 / 30 / 27 / 25 passes per sweep),
+// cfg 3 9.3 / 9.8 / 9.8 at 40 / 48 / 56 (its passes reach the slot cap first).
+constexpr int kRegPassGates = 64;
 // States this large (per shard) stream HBM: generated kernels use 12-qubit tiles
 // (a narrower reverse tile gets a forward schedule over k+1-qubit tiles).
 constexpr int kWideTileQubits = 24;
@@ -748,6 +752,18 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   else if (L.reg)
     pp.max_items = kRegPassGates;
   pp.windows = e->opt_windows != 0;
+  // Generated reverse kernels keep one inner-product accumulator per (slot, thread)
+  // in shared memory next to the transpose tiles; past that budget lanes are
+  // combined per op (a butterfly step each, measured 8 % per halving): cap the
+  // parametrised gates of a pass at what fits (46 at k = 12 / 11 with R = 4).
+  if (jit_planned && L.reg && e->opt_slot_cap) {
+    const int threads = 32 << (L.k - 5 - RB);
+    const int blocks = std::max(1, std::min(2, 256 / threads));
+    const size_t share = std::min<size_t>(e->max_smem, size_t(e->max_smem_sm) / blocks - 1024);
+    const size_t tiles_b = (sizeof(double2) << L.k) * 2;
+    const size_t per_slot = size_t(threads) * sizeof(double) + sizeof(double2) * (threads / 32);
+    if (share > tiles_b + 8 * per_slot) pp.max_derivs = std::min<int>(pp.max_derivs, int((share - tiles_b) / per_slot));
+  }
   const int64_t S = int64_t(16) << nloc;  // bytes of one state shard
 
   std::vector<GateShape> logical(p->num_gates);
@@ -2186,6 +2202,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "jit") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "jit must be 0 (off), 1 (auto) or 2 (always)");
     e->opt_jit = value;
+  } else if (k == "slot_cap") {
+    e->opt_slot_cap = value != 0;
   } else if (k == "pass_windows") {
     e->opt_windows = value != 0;
   } else if (k == "max_gates_per_pass") {

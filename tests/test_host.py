@@ -84,6 +84,26 @@ def test_plan_fuses_full_size_configs():
         assert passes < w.num_gates / 4, (cfg, passes)
 
 
+def test_window_planner_cuts_hbm_passes():
+    """The engine's plan at full size without a GPU (svg_debug_plan_stats): passes over
+    windows of contiguous qubits hold parallelograms of the layered circuits, so
+    cfg 4 (n = 30) needs about half the HBM passes of the layer-by-layer greedy plan,
+    no pass exceeds the per-thread accumulator budget, and every gate is placed once."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from plan_stats import stats
+
+    new, old = stats(4, None, windows=1), stats(4, None, windows=0)
+    for d in ("fwd", "rev"):
+        assert new[d]["reg_ops"] == old[d]["reg_ops"] == new["gates"] == 1424
+        assert new[d]["passes"] <= 30 < 50 <= old[d]["passes"], (new[d], old[d])
+    assert new["rev"]["lane_group_acc"] == 0 and new["rev"]["max_slots"] <= 46
+    c3 = stats(3, None, windows=1)
+    assert c3["rev"]["passes"] <= 48 and c3["rev"]["lane_group_acc"] == 0
+
+
 def test_pauli_lowering_of_rotations():
     """a I + b P of the tables equals the reference closed form cos(at) I + i sin(at) P."""
     from paper_2009_02823_b200.ir import bound_matrix, pauli_product
