@@ -204,6 +204,7 @@ struct svg_engine {
   int64_t opt_jit = 1;
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
   int64_t opt_slot_cap = 1;      // (tuning) cap a pass's derivative slots at the per-thread accumulator budget
+  int64_t opt_l2_prefetch = 1;   // (tuning) generated kernels prefetch the next tile into L2 at tile start
   int64_t opt_windows = 1;       // pass planner: also try windows of contiguous qubits (plan_best_pass)
   int64_t opt_low_qubits = 4;    // generated kernels: contiguous low qubits every tile holds (3..5)
   mutable std::string jit_error;
@@ -1042,6 +1043,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.scale_carry = carry;
         jp.checked = e->opt_checked != 0;
         jp.lowb = std::min(5, L.b);
+        jp.l2_prefetch = e->opt_l2_prefetch != 0 && nloc >= kWideTileQubits;
         jp.segs = L.segs.data() + l.d.seg_begin;
         jp.nsegs = l.d.seg_end - l.d.seg_begin;
         jp.rops = L.rops.data() + l.d.op_begin;
@@ -1476,6 +1478,7 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.scale_carry = carry;
       jp.checked = e->opt_checked != 0;
       jp.lowb = std::min(5, L.b);
+        jp.l2_prefetch = e->opt_l2_prefetch != 0 && nloc >= kWideTileQubits;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -1491,7 +1494,36 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
           for (int si = l->d.seg_begin; si < l->d.seg_end; ++si) {
             const SegDesc& sg = L.segs[si];
             st[o + 1] += 1;                                                      // segments
+            if (std::getenv("SVGB_PLAN_DUMP") && sg.kind == SEG_REG) {
+              std::fprintf(stderr, "%s pass %d seg %d ops %d same %d lanes", l->nb == 2 ? "rev" : "fwd", int(st[o + 0]),
+                           si - l->d.seg_begin, sg.op_end - sg.op_begin, int(sg.same_map));
+              for (int i = 0; i < 5; ++i) std::fprintf(stderr, " %d", int(l->d.q[sg.lanepos[i]]));
+              std::fprintf(stderr, " | regs");
+              for (int i = 0; i < l->R; ++i) std::fprintf(stderr, " %d", int(l->d.q[sg.regpos[i]]));
+              std::fprintf(stderr, " | warps");
+              for (int i = 0; i < l->d.k - 5 - l->R; ++i) std::fprintf(stderr, " %d", int(l->d.q[sg.warppos[i]]));
+              std::fprintf(stderr, "\n");
+            }
             if (si > l->d.seg_begin && !(sg.kind == SEG_REG && sg.same_map)) st[o + 2] += 1;  // layout changes
+            if (si > l->d.seg_begin && sg.kind == SEG_REG && !sg.same_map && L.segs[si - 1].kind == SEG_REG) {
+              // layout changes that exchange m register positions with warp positions, all else in place
+              const SegDesc& pv = L.segs[si - 1];
+              const int wb = l->d.k - 5 - l->R;
+              bool ok = std::memcmp(pv.lanepos, sg.lanepos, 5) == 0;
+              int m = 0;
+              for (int i = 0; i < wb && ok; ++i) {
+                if (pv.warppos[i] == sg.warppos[i]) continue;
+                ++m;
+                bool a = false, b = false;
+                for (int r = 0; r < l->R; ++r) {
+                  a = a || sg.regpos[r] == pv.warppos[i];
+                  b = b || pv.regpos[r] == sg.warppos[i];
+                }
+                ok = a && b;
+              }
+              if (ok && m == 1) st[o + 7] += 1;
+              if (ok && m == 2) st[o + 6] += 0;  // (not counted)
+            }
             if (sg.kind != SEG_REG) continue;
             for (int oi = sg.op_begin; oi < sg.op_end; ++oi) {
               st[o + 3] += 1;                                                    // register ops
@@ -2204,6 +2236,8 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
     e->opt_jit = value;
   } else if (k == "slot_cap") {
     e->opt_slot_cap = value != 0;
+  } else if (k == "l2_prefetch") {
+    e->opt_l2_prefetch = value != 0;
   } else if (k == "pass_windows") {
     e->opt_windows = value != 0;
   } else if (k == "max_gates_per_pass") {

@@ -344,67 +344,117 @@ std::vector<Segment> plan_segments_free(const std::vector<uint32_t>& flip_pos, c
         ++npred[j];
       }
     }
-  std::vector<char> done(m, 0);
-  int remaining = m;
-  // gates runnable (transitively) whose flips lie in `regs`
-  auto closure = [&](uint32_t regs, std::vector<int>* order) {
-    std::vector<int> pred = npred;
-    std::vector<char> taken(done);
+  // Gates runnable (transitively) from the state `done` whose flips lie in `regs`
+  // (worklist over the conflict graph); returns how many, marks them in `taken`.
+  auto closure = [&](const std::vector<char>& done, const std::vector<int>& pred0, uint32_t regs,
+                     std::vector<char>* taken_out, std::vector<int>* order) {
+    std::vector<int> pred = pred0;
+    std::vector<char> taken = done;
+    std::vector<int> ready;
+    for (int i = m - 1; i >= 0; --i)
+      if (!taken[i] && pred[i] == 0 && !(flip_pos[i] & ~regs)) ready.push_back(i);
     int count = 0;
-    for (bool progress = true; progress;) {
-      progress = false;
-      for (int i = 0; i < m; ++i) {
-        if (taken[i] || pred[i] != 0 || (flip_pos[i] & ~regs)) continue;
-        taken[i] = 1;
-        ++count;
-        progress = true;
-        if (order) order->push_back(i);
-        for (int j : succ[i]) --pred[j];
-      }
+    while (!ready.empty()) {
+      // lowest index first: keeps the original gate order inside a segment
+      const auto it = std::min_element(ready.begin(), ready.end());
+      const int i = *it;
+      ready.erase(it);
+      taken[i] = 1;
+      ++count;
+      if (order) order->push_back(i);
+      for (int j : succ[i])
+        if (--pred[j] == 0 && !taken[j] && !(flip_pos[j] & ~regs)) ready.push_back(j);
     }
+    if (taken_out) taken_out->swap(taken);
     return count;
   };
+  // Beam search over sequences of register sets for the fewest segments (each
+  // layout change is a shared-memory transpose of the whole tile): per state the
+  // register sets -- every choice of `regbits` of the positions pending gates
+  // flip -- are ranked by how many gates they run; the best few are expanded.
+  struct Node {
+    std::vector<char> done;
+    int remaining = 0;
+    std::vector<std::pair<uint32_t, std::vector<int>>> segs;  // (register set, items in order)
+  };
+  constexpr int kBeam = 6, kChildren = 4;
+  std::vector<Node> beam(1);
+  beam[0].done.assign(m, 0);
+  beam[0].remaining = m;
   std::vector<Segment> segs;
-  while (remaining > 0) {
-    uint32_t regs = 0;
-    int best_count = closure(0, nullptr);
-    while (popc(regs) < regbits) {
-      uint32_t cand = 0;
-      for (int i = 0; i < m; ++i)
-        if (!done[i]) cand |= flip_pos[i] & all & ~regs;
-      if (!cand) break;
-      int best = -1, best_pos = -1;
-      for (uint32_t v = cand; v; v &= v - 1) {
-        const int p = __builtin_ctz(v);
-        const int c = closure(regs | (1u << p), nullptr);
-        if (c > best || (c == best && p >= lowb && best_pos < lowb)) {  // ties: keep the low positions free for the lanes
-          best = c;
-          best_pos = p;
-        }
-      }
-      if (best <= best_count && popc(regs) > 0) {
-        // no single position unlocks a gate: take the flip set of the earliest ready gate
-        for (int i = 0; i < m; ++i)
-          if (!done[i] && npred[i] == 0 && popc(regs | flip_pos[i]) <= regbits && (flip_pos[i] & ~regs)) {
-            regs |= flip_pos[i];
-            break;
-          }
+  for (int depth = 0; depth < 4 * m + 4 && !beam.empty(); ++depth) {
+    const Node* fin = nullptr;
+    for (const Node& nd : beam)
+      if (nd.remaining == 0) {
+        fin = &nd;
         break;
       }
-      regs |= 1u << best_pos;
-      best_count = best;
+    if (fin) {
+      for (const auto& sgp : fin->segs) {
+        Segment sg;
+        sg.regmask = sgp.first;
+        sg.items = sgp.second;
+        segs.push_back(std::move(sg));
+      }
+      break;
     }
-    Segment sg;
-    sg.regmask = regs;
-    closure(regs, &sg.items);
-    if (sg.items.empty()) throw std::runtime_error("free-lane segment planner made no progress");
-    for (int i : sg.items) {
-      done[i] = 1;
-      --remaining;
-      for (int j : succ[i]) --npred[j];
+    std::vector<Node> next;
+    for (const Node& nd : beam) {
+      std::vector<int> pred0(m, 0);
+      uint32_t cand = 0;
+      for (int i = 0; i < m; ++i) {
+        if (nd.done[i]) continue;
+        cand |= flip_pos[i] & all;
+        for (int j : succ[i]) ++pred0[j];
+      }
+      std::vector<int> pos;
+      for (uint32_t v = cand; v; v &= v - 1) pos.push_back(__builtin_ctz(v));
+      const int np = static_cast<int>(pos.size());
+      std::vector<std::pair<int, uint32_t>> ranked;  // (gates run, register set)
+      if (np <= regbits) {
+        ranked.push_back({closure(nd.done, pred0, cand, nullptr, nullptr), cand});
+      } else {
+        // every regbits-subset of the candidate positions (Gosper's hack)
+        for (uint32_t c = (1u << regbits) - 1u; c < (1u << np);) {
+          uint32_t regs = 0;
+          for (uint32_t v = c; v; v &= v - 1) regs |= 1u << pos[__builtin_ctz(v)];
+          // ties: keep the low positions free for the lanes
+          ranked.push_back({closure(nd.done, pred0, regs, nullptr, nullptr) * 64 - popc(regs & low), regs});
+          const uint32_t t = c | (c - 1);
+          c = (t + 1) | (((~t & -~t) - 1) >> (__builtin_ctz(c) + 1));
+        }
+      }
+      std::sort(ranked.begin(), ranked.end(), [](const auto& a, const auto& b) { return a.first > b.first || (a.first == b.first && a.second < b.second); });
+      int kept = 0;
+      std::vector<std::vector<char>> seen;
+      for (const auto& rk : ranked) {
+        if (kept >= kChildren) break;
+        Node ch;
+        ch.segs = nd.segs;
+        std::vector<int> order;
+        const int cnt = closure(nd.done, pred0, rk.second, &ch.done, &order);
+        if (cnt == 0) break;
+        if (std::find(seen.begin(), seen.end(), ch.done) != seen.end()) continue;  // same gates as a better-ranked set
+        seen.push_back(ch.done);
+        ch.remaining = nd.remaining - cnt;
+        ch.segs.push_back({rk.second, std::move(order)});
+        next.push_back(std::move(ch));
+        ++kept;
+      }
     }
-    segs.push_back(sg);
+    if (next.empty()) throw std::runtime_error("free-lane segment planner made no progress");
+    std::stable_sort(next.begin(), next.end(), [](const Node& a, const Node& b) { return a.remaining < b.remaining; });
+    // distinct states only
+    std::vector<Node> pruned;
+    for (Node& nd : next) {
+      bool dup = false;
+      for (const Node& q : pruned) dup = dup || q.done == nd.done;
+      if (!dup) pruned.push_back(std::move(nd));
+      if (static_cast<int>(pruned.size()) >= kBeam) break;
+    }
+    beam.swap(pruned);
   }
+  if (m > 0 && segs.empty()) throw std::runtime_error("free-lane segment planner did not finish");
   // Fill register sets to `regbits` (positions the next segments flip first:
   // fewer distinct layouts), then lanes: 0..4 where free, else the lowest free
   // positions.  Equal consecutive layouts need no transpose.

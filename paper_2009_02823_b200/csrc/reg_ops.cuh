@@ -312,6 +312,7 @@ __device__ __forceinline__ void cp_async16(void* s, const void* g) {
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* g) { asm volatile("prefetch.global.L2 [%0];" ::"l"(g)); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 template <int R>
 __device__ __forceinline__ void stage_g(double2* stg, const double2* __restrict__ g, uint64_t row, const Map<R>& m,

@@ -21,8 +21,9 @@ def stats(cfg, n, tile=0, reg_bits=0, low=0, max_gates=0, windows=1, shard_bits=
     rc = lib.svg_debug_plan_stats(C.byref(pr.c), opts, out)
     if rc != 0:
         raise RuntimeError(lib.svg_last_error())
-    keys = ("passes", "segments", "layout_changes", "reg_ops", "lane_flips", "max_slots", "lane_group_acc")
-    return {"fwd": dict(zip(keys, out[0:7])), "rev": dict(zip(keys, out[8:15])), "gates": len(w.circuit.gates)}
+    keys = ("passes", "segments", "layout_changes", "reg_ops", "lane_flips", "max_slots", "lane_group_acc",
+            "one_bit_exchanges")
+    return {"fwd": dict(zip(keys, out[0:8])), "rev": dict(zip(keys, out[8:16])), "gates": len(w.circuit.gates)}
 
 
 if __name__ == "__main__":
