@@ -203,8 +203,7 @@ struct svg_engine {
   // >= kJitMinQubits qubits), 2 always
   int64_t opt_jit = 1;
   int64_t opt_tile_fwd = 0;      // forward-only tile qubits (one shard, generated kernels): 0 auto (k+1), -1 off
-  int64_t opt_slot_cap = 1;      // (tuning) cap a pass's derivative slots at the per-thread accumulator budget
-  int64_t opt_l2_prefetch = 1;   // (tuning) generated kernels prefetch the next tile into L2 at tile start
+  int64_t opt_slot_cap = 1;      // cap a pass's derivative slots at the per-thread accumulator budget
   int64_t opt_windows = 1;       // pass planner: also try windows of contiguous qubits (plan_best_pass)
   int64_t opt_low_qubits = 4;    // generated kernels: contiguous low qubits every tile holds (3..5)
   mutable std::string jit_error;
@@ -497,6 +496,9 @@ constexpr int kJitMinQubits = 10;
 // 1.05 / 1.06 gradients/s at 44 / 48 / 64 / 72 (36 / 30 / 27 / 25 passes per sweep),
 // cfg 3 9.3 / 9.8 / 9.8 at 40 / 48 / 56 (its passes reach the slot cap first).
 constexpr int kRegPassGates = 64;
+// Forward passes (psi only, no accumulators, a third of the arithmetic per gate) on
+// their own schedule: measured cfg 4 forward 226 / 204 / 207 / 209 ms at 64 / 80 / 96 / 128.
+constexpr int kFwdPassGates = 80;
 // States this large (per shard) stream HBM: generated kernels use 12-qubit tiles
 // (a narrower reverse tile gets a forward schedule over k+1-qubit tiles).
 constexpr int kWideTileQubits = 24;
@@ -801,21 +803,22 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
   // leaves room for 2^(k+1) amplitudes per CTA: fewer HBM passes.
   int kf = L.k;
   std::shared_ptr<const std::pair<std::vector<Step>, std::vector<int>>> sched_f;
-  // (auto: states of >= kWideTileQubits qubits, whose passes stream HBM; smaller,
-  // L2-resident states are better served by more, smaller tiles -- measured cfg 2)
-  if (g == 0 && jit_planned && nloc > L.k &&
-      (e->opt_tile_fwd > 0 || (e->opt_tile_fwd == 0 && nloc >= kWideTileQubits && L.k <= 11))) {
-    kf = e->opt_tile_fwd > 0 ? static_cast<int>(e->opt_tile_fwd) : L.k + 1;
-    kf = std::max(L.k, std::min({kf, nloc, 13}));
-    if (kf > L.k) {
-      PlanParams pq = pp;
-      pq.k = kf;
-      sched_f = schedule(pq, nullptr);
-    } else {
-      kf = L.k;
+  // (wider tiles, auto: states of >= kWideTileQubits qubits, whose passes stream HBM,
+  // when the reverse tile is narrower than 12; smaller, L2-resident states are better
+  // served by more, smaller tiles -- measured cfg 2).  The forward passes also carry no
+  // inner-product accumulators, so the slot cap does not apply to them.
+  if (g == 0 && jit_planned && nloc > L.k) {
+    if (e->opt_tile_fwd > 0 || (e->opt_tile_fwd == 0 && nloc >= kWideTileQubits && L.k <= 11)) {
+      kf = e->opt_tile_fwd > 0 ? static_cast<int>(e->opt_tile_fwd) : L.k + 1;
+      kf = std::max(L.k, std::min({kf, nloc, 13}));
     }
+    PlanParams pq = pp;
+    pq.k = kf;
+    pq.max_derivs = 1 << 20;
+    if (e->opt_max_items <= 0) pq.max_items = kFwdPassGates;
+    if (nloc >= kWideTileQubits || kf > L.k) sched_f = schedule(pq, nullptr);
   }
-  const std::vector<Step>& fsteps = kf > L.k ? sched_f->first : steps;
+  const std::vector<Step>& fsteps = sched_f ? sched_f->first : steps;
   // physical gates per pass step, parallel to the step's items
   std::vector<GateList> pgates(steps.size());
   std::deque<svg_gate> pstore;  // remapped copies (only when the qubit map is not the identity)
@@ -1043,7 +1046,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.scale_carry = carry;
         jp.checked = e->opt_checked != 0;
         jp.lowb = std::min(5, L.b);
-        jp.l2_prefetch = e->opt_l2_prefetch != 0 && nloc >= kWideTileQubits;
         jp.segs = L.segs.data() + l.d.seg_begin;
         jp.nsegs = l.d.seg_end - l.d.seg_begin;
         jp.rops = L.rops.data() + l.d.op_begin;
@@ -1478,7 +1480,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.scale_carry = carry;
       jp.checked = e->opt_checked != 0;
       jp.lowb = std::min(5, L.b);
-        jp.l2_prefetch = e->opt_l2_prefetch != 0 && nloc >= kWideTileQubits;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;
@@ -2234,12 +2235,6 @@ int svg_engine_set_option(svg_engine* e, const char* key, int64_t value) {
   } else if (k == "jit") {
     if (value < 0 || value > 2) return fail(SVG_EINVAL, "jit must be 0 (off), 1 (auto) or 2 (always)");
     e->opt_jit = value;
-  } else if (k == "slot_cap") {
-    e->opt_slot_cap = value != 0;
-  } else if (k == "l2_prefetch") {
-    e->opt_l2_prefetch = value != 0;
-  } else if (k == "pass_windows") {
-    e->opt_windows = value != 0;
   } else if (k == "max_gates_per_pass") {
     if (value < 0) return fail(SVG_EINVAL, "max_gates_per_pass must be >= 0");
     e->opt_max_items = value;
