@@ -1081,10 +1081,10 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
 
   SVGB_PHASE(4);
   // observable passes keep 11-qubit tiles next to 12-qubit gate passes (their
-  // per-term work is light: more, smaller tiles balance better -- measured cfg 3)
+  // per-term work is light: more, smaller tiles balance better -- measured cfg 3;
+  // cfg 4: 45 / 56 / 93 ms at 11 / 12 / 13 tile qubits, although 13 saves a pass)
   PlanParams pp_obs = pp;
   if (jit_planned && L.k == 12 && e->opt_tile == 0) pp_obs.k = 11;
-  if (const char* ok = std::getenv("SVGB_OBS_K")) pp_obs.k = std::min(nloc, std::atoi(ok));
   const int kobs = pp_obs.k;
   // observable passes: terms in the final physical layout, grouped by the flip
   // pattern on rank bits (a nonzero pattern reads the partner shard's psi), then
