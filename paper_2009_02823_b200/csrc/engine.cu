@@ -227,6 +227,12 @@ struct svg_engine {
   NcclComm comm = nullptr;
   cudaEvent_t ev[6] = {};
   cudaEvent_t blob_ev = nullptr;  // the last table upload from the pinned staging buffer
+  // chunked host input (one shard, >= kChunkMinQubits): copies on their own stream,
+  // one event per chunk; the leading forward passes run chunk by chunk behind them
+  static constexpr int kInputChunks = 16;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[kInputChunks] = {};
+  cudaEvent_t enter_ev = nullptr;
 };
 
 namespace {
@@ -502,6 +508,12 @@ constexpr int kFwdPassGates = 80;
 // States this large (per shard) stream HBM: generated kernels use 12-qubit tiles
 // (a narrower reverse tile gets a forward schedule over k+1-qubit tiles).
 constexpr int kWideTileQubits = 24;
+// Host input states of at least this many qubits (one shard) are copied in chunks with
+// the leading forward passes pipelined behind the copy (SVGB_CHUNK_MIN_QUBITS overrides: tests).
+inline int chunk_min_qubits() {
+  if (const char* v = std::getenv("SVGB_CHUNK_MIN_QUBITS")) return std::max(16, std::atoi(v));
+  return 26;
+}
 // Segment-plan cost model in register-op units (a register rotation = 1): a lane
 // flip is a warp shuffle of both buffers (forward: one), a layout change a
 // shared-memory transpose.  Measured with tools/pass_model.py (round 1).
@@ -1653,15 +1665,37 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     // A host input state starts its (large) host -> device copy before the host-side
     // lowering, which then overlaps the transfer; shards are consecutive slices of
     // the full index range (identity layout at the start).
-    bool input_copied = false;
+    bool input_copied = false, chunked = false;
     if (p->input_amps) {
       const size_t amps0 = (size_t(1) << (p->num_qubits - e->shard_bits)) * e->shards_local;
       // SVG_FLAG_INPUT_LOCAL: the host array is this rank's slice only (no 2^n host copy per rank)
       const size_t first0 = (e->comm && !(p->flags & SVG_FLAG_INPUT_LOCAL))
                                 ? size_t(e->rank) * (size_t(1) << (p->num_qubits - e->shard_bits)) : 0;
       e->psi.reserve(amps0 * sizeof(double2));
-      CK(cudaMemcpyAsync(e->psi.ptr, p->input_amps + first0, amps0 * sizeof(double2), cudaMemcpyHostToDevice,
-                         e->stream));
+      // One shard of >= kChunkMinQubits qubits with generated kernels: the copy goes out
+      // in kInputChunks chunks on its own stream, and the leading forward passes (those
+      // whose tile qubits all lie below the chunk boundary) follow it chunk by chunk
+      // (fwd_cb below) instead of waiting for the whole 16 * 2^n bytes.
+      chunked = e->shards_local == 1 && !e->comm && e->opt_jit != 0 && p->num_qubits >= chunk_min_qubits();
+      if (chunked) {
+        if (!e->copy_stream) {
+          CK(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&e->enter_ev, cudaEventDisableTiming));
+          for (cudaEvent_t& ev : e->chunk_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(e->ev[0], e->stream));  // the timed region starts with the copy
+        CK(cudaEventRecord(e->enter_ev, e->stream));
+        CK(cudaStreamWaitEvent(e->copy_stream, e->enter_ev, 0));
+        const size_t camps = amps0 / svg_engine::kInputChunks;
+        for (int c = 0; c < svg_engine::kInputChunks; ++c) {
+          CK(cudaMemcpyAsync(static_cast<double2*>(e->psi.ptr) + c * camps, p->input_amps + c * camps,
+                             camps * sizeof(double2), cudaMemcpyHostToDevice, e->copy_stream));
+          CK(cudaEventRecord(e->chunk_ev[c], e->copy_stream));
+        }
+      } else {
+        CK(cudaMemcpyAsync(e->psi.ptr, p->input_amps + first0, amps0 * sizeof(double2), cudaMemcpyHostToDevice,
+                           e->stream));
+      }
       input_copied = true;
     }
     // One shard: the initial state is set up before the lowering, and the forward
@@ -1673,21 +1707,22 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
     if (early) {
       const size_t amps0 = size_t(1) << p->num_qubits;
       e->psi.reserve(amps0 * sizeof(double2));
-      CK(cudaEventRecord(e->ev[0], e->stream));
+      if (!chunked) CK(cudaEventRecord(e->ev[0], e->stream));
       if (!p->input_amps) {
         CK(cudaMemsetAsync(e->psi.ptr, 0, amps0 * sizeof(double2), e->stream));
         launch_set_basis(static_cast<double2*>(e->psi.ptr), static_cast<uint64_t>(p->input_basis), e->stream);
         ++early_launches;
       }
-      CK(cudaEventRecord(e->ev[1], e->stream));
+      if (!chunked) CK(cudaEventRecord(e->ev[1], e->stream));
       fwd_cb = [&](Lowered& Lf) {
         double2* psi0 = static_cast<double2*>(e->psi.ptr);
-        for (const Launch& l : Lf.fwd) {
-          const JitArgsHead head{psi0, nullptr, nullptr, nullptr, nullptr, l.d.part_off, 0};
+        const int nq = p->num_qubits;
+        auto launch_range = [&](const Launch& l, uint64_t t0, uint64_t t1) {
+          const JitArgsHead head{psi0, nullptr, nullptr, nullptr, nullptr, l.d.part_off, 0, t0, t1};
           std::vector<unsigned char> args =
               jit_args(*l.jit, head, Lf.segs.data() + l.d.seg_begin, Lf.rops.data() + l.d.op_begin);
           cudaLaunchConfig_t cfg = {};
-          cfg.gridDim = dim3(l.grid);
+          cfg.gridDim = dim3(static_cast<unsigned>(std::min<uint64_t>(l.grid, t1 - t0)));
           cfg.blockDim = dim3(l.threads);
           cfg.dynamicSmemBytes = l.smem;
           cfg.stream = e->stream;
@@ -1699,7 +1734,28 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
           void* params[] = {args.data()};
           CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(l.jit->fn), params));
           ++early_launches;
+        };
+        size_t lead = 0;  // leading passes whose tiles lie inside one input chunk
+        if (chunked) {
+          const int cq = nq - 4;  // log2(amplitudes per chunk); kInputChunks == 16
+          while (lead < Lf.fwd.size()) {
+            const PassDesc& d = Lf.fwd[lead].d;
+            bool inside = true;
+            for (int i = 0; i < d.k; ++i) inside = inside && d.q[i] < cq;
+            if (!inside) break;
+            ++lead;
+          }
+          for (int c = 0; c < svg_engine::kInputChunks; ++c) {
+            CK(cudaStreamWaitEvent(e->stream, e->chunk_ev[c], 0));
+            for (size_t i = 0; i < lead; ++i) {
+              const uint64_t per = uint64_t(1) << (cq - Lf.fwd[i].d.k);  // tiles per chunk
+              launch_range(Lf.fwd[i], c * per, (c + 1) * per);
+            }
+          }
+          CK(cudaEventRecord(e->ev[1], e->stream));
         }
+        for (size_t i = lead; i < Lf.fwd.size(); ++i)
+          launch_range(Lf.fwd[i], 0, uint64_t(1) << (nq - Lf.fwd[i].d.k));
         CK(cudaEventRecord(e->ev[2], e->stream));
       };
     }
@@ -1713,8 +1769,14 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
       // kernels; psi is set up again (early forward launches may have run)
       e->jit_error = ex.what();
       L = lower(e, p, with_reverse, {}, true);
+      if (chunked) CK(cudaStreamWaitEvent(e->stream, e->chunk_ev[svg_engine::kInputChunks - 1], 0));
+      chunked = false;
       init_done = false;
       input_copied = false;
+    }
+    if (chunked && !L.fwd_early) {  // no early forward launches: the stream waits for the whole copy
+      CK(cudaStreamWaitEvent(e->stream, e->chunk_ev[svg_engine::kInputChunks - 1], 0));
+      CK(cudaEventRecord(e->ev[1], e->stream));
     }
     const auto t_lowered = std::chrono::steady_clock::now();
     const int nloc = L.nloc;
@@ -1861,7 +1923,7 @@ int run(svg_engine* e, const svg_problem* p, bool with_reverse, svg_c128* sums_o
         launch_pass_reg(l.nb, l.R, d, l.grid, l.threads, l.smem, s, b0, b1, dsegs, drops, dops, dcoef, prt);
         return;
       }
-      const JitArgsHead head{b0, b1, dops, dcoef, prt, d.part_off, d.rank_bits};
+      const JitArgsHead head{b0, b1, dops, dcoef, prt, d.part_off, d.rank_bits, 0, uint64_t(1) << (nloc - d.k)};
       std::vector<unsigned char> args =
           jit_args(*l.jit, head, L.segs.data() + d.seg_begin, L.rops.data() + d.op_begin);
       launch_generated(l.jit->fn, l.grid, l.threads, l.smem, s, args);
@@ -2198,6 +2260,10 @@ int svg_engine_destroy(svg_engine* e) {
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   if (e->blob_ev) cudaEventDestroy(e->blob_ev);
+  for (cudaEvent_t ev : e->chunk_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->enter_ev) cudaEventDestroy(e->enter_ev);
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
   delete e;
   return SVG_OK;

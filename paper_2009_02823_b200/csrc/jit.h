@@ -86,6 +86,7 @@ struct JitArgsHead {
   double2* partials;
   int64_t part_off;
   uint64_t rank_bits;
+  uint64_t t0, t1;  // tile range of this launch: [0, 2^(nloc-k)) or one chunk of it
 };
 
 // Parameter block of a generated observable pass (then double c[]).

@@ -428,3 +428,28 @@ def test_random_circuit_non_hermitian_matches_oracle():
     vals, energy, _ = oracle.non_hermitian_values(circ, theta, obs, inp.amplitudes)
     assert max_err(rep.values, vals) <= GRAD_TOL
     assert abs(rep.energy - energy) <= ENERGY_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n", [(4, 22), (3, 20), (5, 21)])
+def test_chunked_host_input_pipelines_leading_forward_passes(cfg, n, monkeypatch):
+    """Large host inputs are copied in 16 chunks with the leading forward passes (tile
+    qubits below the chunk boundary) launched chunk by chunk behind the copy: same
+    kernels, same tiles -- the result is bitwise the one of the plain copy, and matches
+    the oracle.  (The threshold, 26 qubits, is lowered through the test hook.)"""
+    from cases import random_amplitudes
+    from oracle import oracle
+
+    w = sv.build_workload(cfg, n)
+    inp = sv.StateVector(n, random_amplitudes(n, 17))
+    monkeypatch.delenv("SVGB_CHUNK_MIN_QUBITS", raising=False)
+    plain = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp)
+    monkeypatch.setenv("SVGB_CHUNK_MIN_QUBITS", "16")
+    chunked = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp)
+    again = sv.reverse_mode_gradient(w.circuit, w.theta, w.observable, inp)
+    assert np.array_equal(chunked.values, plain.values) and chunked.energy == plain.energy
+    assert np.array_equal(again.values, plain.values)
+    if n <= 20:
+        vals, energy, _ = oracle.reverse_mode_values(w.circuit, w.theta, w.observable, inp.amplitudes)
+        assert max_err(chunked.values, vals) <= GRAD_TOL
+        assert abs(chunked.energy - energy) <= ENERGY_TOL
