@@ -1058,7 +1058,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
         jp.scale_carry = carry;
         jp.checked = e->opt_checked != 0;
         jp.lowb = std::min(5, L.b);
-        jp.warp_local = std::getenv("SVGB_NO_WARP_LOCAL") == nullptr;
         jp.segs = L.segs.data() + l.d.seg_begin;
         jp.nsegs = l.d.seg_end - l.d.seg_begin;
         jp.rops = L.rops.data() + l.d.op_begin;
@@ -1494,7 +1493,6 @@ Lowered lower(const svg_engine* e, const svg_problem* p, bool with_reverse,
       jp.scale_carry = carry;
       jp.checked = e->opt_checked != 0;
       jp.lowb = std::min(5, L.b);
-        jp.warp_local = std::getenv("SVGB_NO_WARP_LOCAL") == nullptr;
       jp.segs = L.segs.data() + l->d.seg_begin;
       jp.nsegs = l->d.seg_end - l->d.seg_begin;
       jp.rops = L.rops.data() + l->d.op_begin;

@@ -33,7 +33,6 @@ struct JitPass {
   bool scale_carry = false;          // deferred scale carried across layout changes (no shared-memory segments)
   bool checked = false;              // checked mode: shared-memory reads poison what they read, global indices
                                      // bounds-checked (reg_ops.cuh; debugging and tests only)
-  bool warp_local = true;            // lane <-> register layout changes by warp shuffles (no shared memory)
   int lowb = 5;                      // tile positions 0..lowb-1 are qubits 0..lowb-1 (contiguous global rows)
   uint64_t rest = 0;
   const uint8_t* q = nullptr;        // tile qubits (PassDesc.q)
