@@ -186,30 +186,49 @@ std::vector<Step> plan_schedule(const std::vector<GateShape>& logical, int n, in
 
 std::vector<Pass> plan_term_passes(const std::vector<uint64_t>& term_flips, const PlanParams& pp,
                                    std::vector<int>* direct) {
-  std::vector<Pass> passes;
-  std::vector<uint64_t> masks;  // unpadded tile sets
+  // Greedy packing of flip masks into tiles: a pass is seeded with the widest
+  // remaining mask and then takes, one at a time, the term that adds the fewest
+  // new tile qubits (first in term order among equals) until nothing fits.  On
+  // random Pauli sums this needs ~20 % fewer passes than first fit in term order
+  // (cfg 5: 12 instead of 15 at n = 33; every pass but the first moves 3 S).
+  const uint64_t low = low_mask(pp.b);
+  std::vector<int> rem;
   for (int t = 0; t < static_cast<int>(term_flips.size()); ++t) {
-    const uint64_t f = term_flips[t];
-    if (popc(low_mask(pp.b) | f) > pp.k) {  // too wide for a tile: untiled gather pass
-      direct->push_back(t);
-      continue;
-    }
-    int chosen = -1;
-    for (int j = 0; j < static_cast<int>(passes.size()); ++j) {
-      if (popc(masks[j] | f) <= pp.k && static_cast<int>(passes[j].items.size()) < pp.max_items) {
-        chosen = j;
-        break;
-      }
-    }
-    if (chosen < 0) {
-      passes.emplace_back();
-      masks.push_back(low_mask(pp.b));
-      chosen = static_cast<int>(passes.size()) - 1;
-    }
-    masks[chosen] |= f;
-    passes[chosen].items.push_back(t);
+    if (popc(low | term_flips[t]) > pp.k)
+      direct->push_back(t);  // too wide for a tile: untiled gather pass
+    else
+      rem.push_back(t);
   }
-  for (size_t j = 0; j < passes.size(); ++j) passes[j].qmask = pad_tile(masks[j], pp.n, pp.k);
+  std::vector<Pass> passes;
+  while (!rem.empty()) {
+    size_t seed = 0;
+    for (size_t i = 1; i < rem.size(); ++i)
+      if (popc(term_flips[rem[i]] & ~low) > popc(term_flips[rem[seed]] & ~low)) seed = i;
+    Pass p;
+    uint64_t q = low | term_flips[rem[seed]];
+    p.items.push_back(rem[seed]);
+    rem.erase(rem.begin() + seed);
+    while (static_cast<int>(p.items.size()) < pp.max_items) {
+      int best = -1, best_add = 65;
+      for (size_t i = 0; i < rem.size(); ++i) {
+        const int total = popc(q | term_flips[rem[i]]);
+        if (total > pp.k) continue;
+        const int add = total - popc(q);
+        if (add < best_add) {
+          best_add = add;
+          best = static_cast<int>(i);
+          if (add == 0) break;
+        }
+      }
+      if (best < 0) break;
+      q |= term_flips[rem[best]];
+      p.items.push_back(rem[best]);
+      rem.erase(rem.begin() + best);
+    }
+    std::sort(p.items.begin(), p.items.end());  // term order inside a pass (summation order)
+    p.qmask = pad_tile(q, pp.n, pp.k);
+    passes.push_back(std::move(p));
+  }
   return passes;
 }
 
