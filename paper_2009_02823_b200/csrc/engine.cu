@@ -2412,6 +2412,31 @@ extern "C" int svg_debug_plan_stats(const svg_problem* p, const int64_t* opts, d
   }
 }
 
+// Debug / tests (not in the public header): the free-lane segment plan of one pass.
+// flips / touch: tile-local masks of the pass's m gates in order; out_seg[i] = segment
+// of gate i, out_pos[i] = its position inside the segment; regmask / lanemask per segment.
+extern "C" int svg_debug_segments(const uint32_t* flips, const uint32_t* touch, int m, int k, int regbits, int lowb,
+                                  int32_t* out_seg, int32_t* out_pos, uint32_t* regmask, uint32_t* lanemask,
+                                  int32_t* nsegs) {
+  try {
+    const std::vector<uint32_t> f(flips, flips + m), t(touch, touch + m);
+    const std::vector<Segment> segs = plan_segments_free(f, t, k, regbits, lowb);
+    for (int i = 0; i < m; ++i) out_seg[i] = out_pos[i] = -1;
+    for (size_t s = 0; s < segs.size(); ++s) {
+      regmask[s] = segs[s].regmask;
+      lanemask[s] = segs[s].lanemask;
+      for (size_t j = 0; j < segs[s].items.size(); ++j) {
+        out_seg[segs[s].items[j]] = static_cast<int32_t>(s);
+        out_pos[segs[s].items[j]] = static_cast<int32_t>(j);
+      }
+    }
+    *nsegs = static_cast<int32_t>(segs.size());
+    return SVG_OK;
+  } catch (const std::exception& ex) {
+    return fail(SVG_EINVAL, ex.what());
+  }
+}
+
 // Debug / profiling (not in the public header): per-phase host milliseconds of
 // lower() accumulated on the calling thread since the last reset (out_ms[0..8]).
 extern "C" int svg_debug_phase_ms(double* out_ms, int reset) {

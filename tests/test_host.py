@@ -104,6 +104,57 @@ def test_window_planner_cuts_hbm_passes():
     assert c3["rev"]["passes"] <= 48 and c3["rev"]["lane_group_acc"] == 0
 
 
+@pytest.mark.parametrize("k,regbits,lowb", [(12, 4, 4), (11, 4, 5), (12, 3, 4), (10, 4, 3)])
+def test_free_lane_segment_plans_are_valid(k, regbits, lowb):
+    """Beam-search segment planner (plan_segments_free) on random passes of one-qubit-flip
+    gates: every gate lands in exactly one segment, flips only register positions of its
+    segment, conflicting gates keep their order, and the layouts are well formed."""
+    import ctypes as C
+
+    from paper_2009_02823_b200 import _native as N
+
+    lib = N.load()
+    rng = np.random.default_rng([k, regbits, lowb])
+    for trial in range(12):
+        m = int(rng.integers(1, 70))
+        width = int(rng.integers(2, k + 1))  # active tile positions of this pass
+        active = rng.choice(k, size=width, replace=False)
+        flips = np.zeros(m, dtype=np.uint32)
+        touch = np.zeros(m, dtype=np.uint32)
+        for i in range(m):
+            kind = rng.integers(0, 3)
+            t = int(rng.choice(active))
+            if kind == 0:      # rotation with a flip
+                flips[i] = touch[i] = 1 << t
+            elif kind == 1:    # diagonal
+                touch[i] = 1 << t
+            else:              # controlled flip: control is diagonal
+                c = int(rng.choice(active))
+                flips[i] = 1 << t
+                touch[i] = (1 << t) | (1 << c)
+        seg = np.zeros(m, dtype=np.int32)
+        pos = np.zeros(m, dtype=np.int32)
+        regmask = np.zeros(m + 1, dtype=np.uint32)
+        lanemask = np.zeros(m + 1, dtype=np.uint32)
+        nsegs = C.c_int32()
+        rc = lib.svg_debug_segments(flips.ctypes.data_as(C.c_void_p), touch.ctypes.data_as(C.c_void_p), m, k, regbits, lowb,
+                                    seg.ctypes.data_as(C.c_void_p), pos.ctypes.data_as(C.c_void_p),
+                                    regmask.ctypes.data_as(C.c_void_p), lanemask.ctypes.data_as(C.c_void_p),
+                                    C.byref(nsegs))
+        assert rc == 0, lib.svg_last_error()
+        ns = nsegs.value
+        assert 1 <= ns <= m and (seg >= 0).all() and (seg < ns).all()
+        assert len({(int(a), int(b)) for a, b in zip(seg, pos)}) == m
+        for s_ in range(ns):
+            r, l = int(regmask[s_]), int(lanemask[s_])
+            assert bin(r).count("1") == regbits and bin(l).count("1") == 5 and r & l == 0 and (r | l) < (1 << k)
+        for i in range(m):
+            assert int(flips[i]) & ~int(regmask[seg[i]]) == 0
+            for j in range(i + 1, m):
+                if int(touch[i]) & int(touch[j]) & (int(flips[i]) | int(flips[j])):
+                    assert (seg[i], pos[i]) < (seg[j], pos[j]), (trial, i, j)
+
+
 def test_pauli_lowering_of_rotations():
     """a I + b P of the tables equals the reference closed form cos(at) I + i sin(at) P."""
     from paper_2009_02823_b200.ir import bound_matrix, pauli_product
